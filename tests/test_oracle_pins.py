@@ -1,0 +1,403 @@
+"""Pins for the CPU oracle, all `-m "not gpu"`.
+
+Each test pins the oracle to something other than itself: hand-evaluated
+values (tests/golden/), closed forms of classical SOR theory, invariants,
+special cases that reduce to a textbook routine written independently here,
+brute force (dense direct solve, naive per-cell loops).  A plausible mistake
+anywhere in oracle/sor_oracle.c (dropped term, wrong sign, wrong colour
+origin, transposed operand, wrong phase order, wrong cadence) fails at least
+one of them.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import sor_inputs as SI
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------------
+# P1: hand-computed first iteration of C1 (bitwise; dyadic values)
+def _golden_c1():
+    rows = []
+    with open(os.path.join(GOLDEN, "c1_iteration1.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            ph, i, j, v = line.split()
+            rows.append((ph, int(i), int(j), float(v)))
+    return rows
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_p1_c1_first_iteration_hand_values(orc, dtype):
+    cfg = SI.config("C1")
+    u = orc.to_storage(cfg.init(), dtype)
+    gold = _golden_c1()
+    if dtype == "f64":
+        # red phase alone (orc_half_sweep), then black
+        m = orc.half_sweep(u, 0, cfg.omega)
+        for ph, i, j, v in gold:
+            if ph == "red":
+                assert u[i, j] == v, (i, j)
+        m = max(m, orc.half_sweep(u, 1, cfg.omega))
+        for ph, i, j, v in gold:
+            if ph == "black":
+                assert u[i, j] == v, (i, j)
+            if ph == "maxdelta":
+                assert m == v
+    u2 = orc.to_storage(cfg.init(), dtype)
+    rep = orc.iterate(u2, cfg.omega, 1, measure_last=True)
+    assert rep.iters == 1 and rep.half_sweeps == 2
+    for ph, i, j, v in gold:
+        if ph == "black":
+            assert u2[i, j] == v, (dtype, i, j)
+        if ph == "maxdelta":
+            assert rep.max_change == v
+    # ring untouched
+    assert np.array_equal(u2[0], cfg.init()[0].astype(u2.dtype))
+    assert not u2[-1].any() and not u2[1:, 0].any() and not u2[1:, -1].any()
+
+
+# --------------------------------------------------------------------------
+# P2: SPEC worked examples
+def test_p2_cell_update_examples(orc):
+    # X=0, neighbours (1,0,0,0), omega=0.376 -> 0.094
+    assert orc.cell_update(1.0, 0.0, 0.0, 0.0, 0.0, 0.376) == 0.094
+    # omega=1, X=0.5, neighbours (1,1,1,1) -> 1.0 (pure GS iterate)
+    assert orc.cell_update(1.0, 1.0, 1.0, 1.0, 0.5, 1.0) == 1.0
+    # zero neighbourhood is a fixed point for any omega
+    for w in (0.376, 1.0, 1.9):
+        assert orc.cell_update(0.0, 0.0, 0.0, 0.0, 0.0, w) == 0.0
+    # Eq. 1 form omega*Xbar + (1-omega)*X agrees with the BJ form up to rounding
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n, s, w_, e, u = rng.uniform(-10, 10, 5)
+        om = rng.uniform(0.05, 1.95)
+        eq1 = om * ((n + s + w_ + e) / 4.0) + (1.0 - om) * u
+        assert abs(orc.cell_update(n, s, w_, e, u, om) - eq1) <= 1e-13 * 40
+
+
+def test_p2_red_sweep_n4(orc):
+    # n=4 (2x2 interior), north=1, red sweep omega=0.376:
+    # interior red cells adjacent to north become 0.094, black cells stay 0.
+    u = SI.north_hot(2, 2, 1.0)
+    orc.half_sweep(u, 0, 0.376)
+    assert u[1, 1] == 0.094          # (1,1) red, touches north
+    assert u[2, 2] == 0.0            # (2,2) red, not adjacent to north
+    assert u[1, 2] == 0.0 and u[2, 1] == 0.0   # black untouched
+
+
+def test_p2_jacobi_one_step_n4(orc):
+    # one Jacobi step on n=4 north-hot grid -> cells next to north 0.25
+    u = SI.north_hot(2, 2, 1.0)
+    rep = orc.jacobi(u, 1e-300, 1)
+    assert rep.iters == 1
+    assert u[1, 1] == 0.25 and u[1, 2] == 0.25
+    assert u[2, 1] == 0.0 and u[2, 2] == 0.0
+
+
+# --------------------------------------------------------------------------
+# Brute force: naive Code-1 style guarded per-cell sweep
+def _naive_iteration(u, omega):
+    rows, cols = u.shape[0] - 2, u.shape[1] - 2
+    for c in (0, 1):
+        for i in range(rows + 2):
+            for j in range(cols + 2):
+                if i in (0, rows + 1) or j in (0, cols + 1):
+                    continue
+                if (i + j) % 2 == c:          # Code 1: `if ((i+j) % 2 == c)` (reading #14)
+                    s = (u[i - 1, j] + u[i + 1, j]) + (u[i, j - 1] + u[i, j + 1])
+                    u[i, j] = u[i, j] + omega * (0.25 * s - u[i, j])
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (1, 5), (4, 1), (5, 7), (6, 6), (9, 4)])
+def test_stride2_equals_naive_guarded(orc, rows, cols):
+    u = SI.random_field(rows, cols, seed=rows * 100 + cols)
+    v = u.copy()
+    for _ in range(3):
+        _naive_iteration(v, 1.37)
+    orc.iterate(u, 1.37, 3)
+    assert np.array_equal(u, v)
+
+
+# --------------------------------------------------------------------------
+# P3: fixed point = dense direct solve of the 5-point Dirichlet system
+@pytest.mark.parametrize("rows,cols", [(7, 7), (5, 9), (12, 3), (16, 16)])
+def test_p3_converges_to_dense_solution(orc, rows, cols):
+    init = SI.random_edges(rows, cols, seed=rows + 31 * cols)
+    bnd = np.abs(init).max()
+    exact = init.copy()
+    orc.dense_solve(exact)
+    u = init.copy()
+    w = SI.omega_opt(max(rows, cols))
+    rep = orc.solve(u, w, 1e-15 * bnd, 100000)
+    assert rep.converged
+    assert np.abs(u - exact).max() <= 1e-12 * bnd
+
+
+def test_p3_jacobi_and_sor_agree(orc):
+    # converged Jacobi vs converged SOR within 10*eps
+    init = SI.north_hot(15, 15, 1.0)
+    a = init.copy()
+    b = init.copy()
+    ra = orc.jacobi(a, 1e-12, 200000)
+    rb = orc.solve(b, 1.0, 1e-12, 200000)
+    assert ra.converged and rb.converged
+    exact = init.copy()
+    orc.dense_solve(exact)
+    assert np.abs(a - b).max() <= 1e-9
+    assert np.abs(a - exact).max() <= 1e-9
+
+
+# --------------------------------------------------------------------------
+# P4: discrete-harmonic boundary is a fixed point
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("omega", [0.376, 1.0, 1.5, 1.9])
+def test_p4_dyadic_linear_fixed_point_bitwise(orc, dtype, omega):
+    rows, cols = 13, 10
+    i, j = np.meshgrid(np.arange(rows + 2), np.arange(cols + 2), indexing="ij")
+    lin = 0.25 * j + 0.75 * i + 5.0
+    u = orc.to_storage(lin, dtype)
+    ref = u.copy()
+    orc.iterate(u, omega, 200)
+    assert np.array_equal(u, ref)
+
+
+def test_p4_c4_base_drift_and_convergence(orc):
+    rows = cols = 24
+    u = SI.harmonic_edges(rows, cols, noise_seed=None)   # 0.3x + 0.7y + 5, no noise
+    i, j = np.meshgrid(np.arange(rows + 2), np.arange(cols + 2), indexing="ij")
+    exact = 0.3 * (j / (cols + 1)) + 0.7 * (i / (rows + 1)) + 5.0
+    # starting AT the linear function: it is (to rounding) a fixed point
+    v = exact.copy()
+    orc.iterate(v, 1.9, 500)
+    assert np.abs(v - exact).max() <= 1e-13
+    # from interior 0: converges to the linear function
+    rep = orc.solve(u, SI.omega_opt(rows), 1e-14, 100000)
+    assert rep.converged
+    assert np.abs(u - exact).max() <= 1e-12
+
+
+# --------------------------------------------------------------------------
+# P5: omega = 1 is red-black Gauss-Seidel (independent textbook GS in numpy)
+def _textbook_rb_gs(u, iters):
+    rows, cols = u.shape[0] - 2, u.shape[1] - 2
+    i, j = np.meshgrid(np.arange(1, rows + 1), np.arange(1, cols + 1), indexing="ij")
+    for _ in range(iters):
+        for c in (0, 1):
+            m = ((i + j) % 2) == c
+            I, J = i[m], j[m]
+            u[I, J] = 0.25 * ((u[I - 1, J] + u[I + 1, J]) + (u[I, J - 1] + u[I, J + 1]))
+
+
+@pytest.mark.parametrize("n", [17, 18])
+def test_p5_omega1_is_gauss_seidel(orc, n):
+    init = SI.random_edges(n, n, seed=n)
+    bnd = np.abs(init).max()
+    a, b = init.copy(), init.copy()
+    for k in range(40):
+        orc.iterate(a, 1.0, 1)
+        _textbook_rb_gs(b, 1)
+        assert np.abs(a - b).max() <= 1e-13 * bnd, k
+
+
+# --------------------------------------------------------------------------
+# P6: asymptotic convergence factor vs Young's closed form
+def _young_rho(omega, n):
+    mu = math.cos(math.pi / (n + 1))
+    wopt = 2.0 / (1.0 + math.sqrt(1.0 - mu * mu))
+    if omega >= wopt:
+        return omega - 1.0
+    return ((omega * mu + math.sqrt(omega * omega * mu * mu - 4.0 * (omega - 1.0))) / 2.0) ** 2
+
+
+def _delta_history(orc, n, omega, iters, seed=3):
+    u = np.zeros((n + 2, n + 2))
+    u[1:-1, 1:-1] = SI.uniform01(seed, n * n).reshape(n, n)
+    hist = []
+    for _ in range(iters):
+        hist.append(orc.iterate(u, omega, 1, measure_last=True).max_change)
+    return np.array(hist)
+
+
+@pytest.mark.parametrize("n,omega", [(32, 1.0), (32, 1.5), (16, 1.2)])
+def test_p6_rho_below_omega_opt(orc, n, omega):
+    h = _delta_history(orc, n, omega, 2500)
+    ratio = h[-1] / h[-2]
+    assert ratio == pytest.approx(_young_rho(omega, n), rel=2e-5)
+
+
+@pytest.mark.parametrize("n,omega", [(16, None), (32, 1.95), (64, None)])
+def test_p6_rho_at_or_above_omega_opt(orc, n, omega):
+    w = SI.omega_opt(n) if omega is None else omega
+    h = _delta_history(orc, n, w, 700)
+    # complex eigenvalues: the ratio oscillates; use the geometric mean over a window
+    lo, hi = 300, 650
+    gm = (h[hi] / h[lo]) ** (1.0 / (hi - lo))
+    assert h[hi] > 1e-250
+    assert gm == pytest.approx(w - 1.0, rel=5e-3)
+
+
+# --------------------------------------------------------------------------
+# P7: symmetry
+def test_p7_mirror_symmetry_odd_cols(orc):
+    rows, cols = 20, 33
+    u = np.zeros((rows + 2, cols + 2))
+    e = SI.uniform01(11, cols + 2) * 100
+    u[0, :] = (e + e[::-1]) / 2          # left-right symmetric north edge
+    u[1:-1, 0] = u[1:-1, -1] = 7.0
+    orc.iterate(u, 1.7, 60)
+    assert np.array_equal(u, u[:, ::-1])
+
+
+def test_p7_centre_value_odd_n(orc):
+    # four rotated north-hot problems superpose to the all-T solution: centre = T/4
+    n = 33
+    u = SI.north_hot(n, n, 100.0)
+    u[0, 0] = u[0, -1] = 0.0             # corners are never read
+    rep = orc.solve(u, SI.omega_opt(n), 1e-12, 100000)
+    assert rep.converged
+    assert abs(u[17, 17] - 25.0) <= 1e-9
+
+
+def test_p7_even_n_central_cells_sum(orc):
+    n = 32
+    u = SI.north_hot(n, n, 100.0)
+    rep = orc.solve(u, SI.omega_opt(n), 1e-12, 100000)
+    assert rep.converged
+    assert abs(u[16, 16] + u[16, 17] + u[17, 16] + u[17, 17] - 100.0) <= 1e-8
+
+
+# --------------------------------------------------------------------------
+# P8: maximum principle for 0 < omega <= 1
+@pytest.mark.parametrize("omega", [0.376, 0.8, 1.0])
+def test_p8_maximum_principle(orc, omega):
+    u = SI.random_field(23, 17, seed=99)
+    for _ in range(30):
+        orc.iterate(u, omega, 1)
+        assert u.min() >= 0.0 and u.max() <= 1.0
+
+
+# --------------------------------------------------------------------------
+# P9 / P15: cadence and accounting
+def test_p9_zero_problem_converges_at_first_check(orc):
+    u = np.zeros((10, 12))
+    rep = orc.solve(u, 1.5, 1e-6, 100, check_every=7)
+    assert rep.converged and rep.iters == 7 and rep.max_change == 0.0 and rep.checks == 1
+
+
+def test_p15_check_accounting(orc):
+    u = SI.north_hot(8, 8, 1.0)
+    rep = orc.solve(u, 0.376, 1e-300, 20, check_every=7)
+    assert not rep.converged
+    assert rep.iters == 20 and rep.half_sweeps == 40 and rep.checks == 2   # checks at 7 and 14
+
+
+def test_solve_strict_less_than(orc):
+    # equality continues (reading #7): tol equal to the exact max change must not stop
+    cfg = SI.config("C1")
+    u = cfg.init()
+    rep = orc.solve(u, cfg.omega, 65.625, 5)       # iteration-1 change is exactly 65.625
+    assert rep.iters >= 2
+    u = cfg.init()
+    rep = orc.solve(u, cfg.omega, np.nextafter(65.625, 1e9), 5)
+    assert rep.converged and rep.iters == 1
+
+
+def test_oracle_rejects_bad_args(orc):
+    u = np.zeros((5, 5))
+    with pytest.raises(ValueError):
+        orc.solve(u, 2.0, 1e-6, 10)
+    with pytest.raises(ValueError):
+        orc.solve(u, 1.0, 0.0, 10)
+    with pytest.raises(ValueError):
+        orc.solve(u, 1.0, 1e-6, 10, check_every=11)
+
+
+# --------------------------------------------------------------------------
+# P13: fused |delta| == Algorithm 1's snapshot diff, bitwise
+@pytest.mark.parametrize("K", [1, 3, 50])
+def test_p13_fused_delta_equals_snapshot(orc, K):
+    init = SI.random_edges(21, 18, seed=K)
+    a, b = init.copy(), init.copy()
+    ra = orc.solve(a, 1.8, 1e-4, 400, check_every=K)
+    rb = orc.solve_snapshot(b, 1.8, 1e-4, 400, check_every=K)
+    assert (ra.status, ra.iters, ra.checks) == (rb.status, rb.iters, rb.checks)
+    assert ra.max_change == rb.max_change
+    assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------
+# P14: threaded (P workers + barrier per phase) == serial, bitwise
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_p14_threads_equal_serial(orc, dtype, P):
+    init = SI.random_edges(37, 29, seed=P)
+    a, b = orc.to_storage(init, dtype), orc.to_storage(init, dtype)
+    ra = orc.solve(a, 1.9, 1e-3, 300)
+    rb = orc.solve(b, 1.9, 1e-3, 300, threads=P)
+    assert (ra.status, ra.iters, ra.max_change) == (rb.status, rb.iters, rb.max_change)
+    assert np.array_equal(a, b)
+    ia, ib = orc.to_storage(init, dtype), orc.to_storage(init, dtype)
+    orc.iterate(ia, 1.3, 17)
+    orc.iterate(ib, 1.3, 17, threads=P)
+    assert np.array_equal(ia, ib)
+
+
+def test_partition_rows(orc):
+    for rows in (1, 7, 64, 100):
+        for P in (1, 2, 3, 8):
+            if P > rows:
+                continue
+            spans = [orc.partition_rows(rows, P, p) for p in range(P)]
+            assert spans[0][0] == 1 and spans[-1][1] == rows + 1
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+            assert all(spans[p][1] == spans[p + 1][0] for p in range(P - 1))
+
+
+# --------------------------------------------------------------------------
+# slab emulation: a slab with halo rows as its ring, row_off = global offset
+def test_row_offset_slab_equivalence(orc):
+    rows, cols = 20, 11
+    g = SI.random_field(rows, cols, seed=4)
+    ref = g.copy()
+    orc.half_sweep(ref, 0, 1.6)
+    # rows 6..13 (global) as a slab whose ring rows are global rows 5 and 14
+    s = g[5:15].copy()
+    orc.half_sweep(s, 0, 1.6, row_off=5)
+    assert np.array_equal(s[1:-1], ref[6:14])
+
+
+# --------------------------------------------------------------------------
+# fp32: subnormals preserved (reading #17), f32 tracks f64
+def test_f32_subnormals_kept(orc):
+    u = np.zeros((12, 12), dtype=np.float32)
+    u[0, :] = np.float32(2e-38)
+    orc.iterate(u, 1.0, 5)
+    tiny = u[(u != 0) & (np.abs(u) < np.finfo(np.float32).tiny)]
+    assert tiny.size > 0
+
+
+def test_f32_tracks_f64(orc):
+    init = SI.random_edges(30, 30, seed=8)
+    a, b = orc.to_storage(init, "f64"), orc.to_storage(init, "f32")
+    orc.iterate(a, 1.9, 100)
+    orc.iterate(b, 1.9, 100)
+    assert np.abs(a - b.astype(np.float64)).max() <= 1e-4 * 100
+
+
+def test_nan_propagates_in_max(orc):
+    u = SI.north_hot(6, 6, 1.0)
+    u[0, 3] = np.nan
+    rep = orc.iterate(u, 1.0, 1, measure_last=True)
+    assert math.isnan(rep.max_change)
+    u = SI.north_hot(6, 6, 1.0)
+    u[0, 3] = np.nan
+    rep = orc.solve(u, 1.0, 1e-3, 5)
+    assert not rep.converged
