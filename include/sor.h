@@ -1,0 +1,175 @@
+/*
+ * sor.h — C ABI of the B200-native red-black SOR hot path (libsor.so).
+ *
+ * Method: S. Mittal, "A Study of Successive Over-relaxation Method
+ * Parallelization Over Modern HPC Languages", arXiv 1401.0763.
+ * Citation key: P:n = /root/reference/PAPER.md line n (section in brackets);
+ * "reading #k" = DESIGN.md §3 (the interpretation adopted where the paper is
+ * silent or garbled, shared with the oracle but not its code).
+ *
+ * What one iteration computes (every entry point below runs exactly this):
+ *   red phase   [§3.1; Alg. 1 P:313]: for every interior cell
+ *               with (i+j) even, Eq. 1 [§2.1, P:97-100] in the canonical form
+ *               s = (uN+uS)+(uW+uE); a = 0.25*s; r = a - u; u' = u + w*r
+ *               (readings #2-#4; no FMA contraction, no reassociation);
+ *   black phase [P:198, P:316]: the same for (i+j) odd, reading the new reds;
+ *   max-change  [P:103, Alg. 1 P:319-325]: max over interior cells of
+ *               |u' - u| (reading #5), on checked iterations only.
+ * Indices are on the global padded grid: row 0 is the north ring,
+ * cell (1,1) is red (reading #11).  The ring is Dirichlet data, never written.
+ *
+ * Conventions shared by every call:
+ *   - Grid arrays are row-major (rows+2) x (cols+2) fp64 INCLUDING the ring
+ *     (reading #1: rows, cols count interior cells).  Pointers may be host
+ *     memory (pageable or pinned) or device memory of the handle's GPU (e.g.
+ *     a torch tensor's data_ptr); the library detects which.  Caller buffers
+ *     are borrowed only for the duration of the call; the caller keeps
+ *     ownership.
+ *   - Return value: SOR_OK (0) on success, SOR_NOT_CONVERGED (1) when a solve
+ *     reached maxit (outputs and grid still valid), negative sor_status on
+ *     error.  On a negative status, sor_last_error() returns a thread-local
+ *     message.  Invalid arguments (SOR_E_INVAL) leave the handle unchanged.
+ *     A CUDA or NCCL failure (SOR_E_CUDA / SOR_E_NCCL) makes the handle
+ *     sticky-failed: later calls return SOR_E_STATE until sor_destroy.
+ *   - Calls are synchronous: they return after the device work completed.
+ *     A handle is not thread-safe; distinct handles are independent.
+ *   - There is no CPU fallback: without a usable sm_100 GPU, sor_create*
+ *     returns SOR_E_CUDA.
+ */
+#ifndef SOR_H
+#define SOR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sor_grid sor_grid; /* opaque; owns all device memory, stream, events, comm */
+
+typedef enum { SOR_F64 = 0, SOR_F32 = 1 } sor_dtype;
+
+typedef enum {
+  SOR_OK = 0,
+  SOR_NOT_CONVERGED = 1,
+  SOR_E_INVAL = -1,
+  SOR_E_NOMEM = -2,
+  SOR_E_CUDA = -3,
+  SOR_E_NCCL = -4,
+  SOR_E_STATE = -5,
+  SOR_E_UNSUPPORTED = -6
+} sor_status;
+
+/* Kernel variants (selected explicitly; there is no auto-dispatch).  All give
+ * bitwise-identical results.                                  */
+typedef enum {
+  SOR_KERNEL_NATURAL = 1,  /* K1: one launch per colour phase, in place, natural layout */
+  SOR_KERNEL_FUSED = 3,    /* K3: red+black fused in one HBM pass, src->dst ping-pong  */
+  SOR_KERNEL_TEMPORAL = 4, /* K4: T iterations per HBM pass (temporal blocking)         */
+  SOR_KERNEL_SMALL = 5     /* K5: whole grid in one CTA's shared memory, one launch     */
+} sor_kernel;
+
+/* Create a single-GPU handle on the current CUDA device.
+ *   N / rows, cols : interior size, >= 1 each (reading #1).
+ *   init           : (rows+2)*(cols+2) fp64, row-major, host or device; ring =
+ *                    Dirichlet data, interior = initial guess; all finite.
+ *   dt             : storage AND arithmetic type.  SOR_F32 rounds init to
+ *                    nearest once; w and 0.25 are rounded once (reading #17).
+ * Default kernel: SOR_KERNEL_FUSED.  Returns SOR_E_INVAL (NULL out/init,
+ * rows/cols < 1, non-finite init), SOR_E_NOMEM, SOR_E_CUDA.                 */
+int sor_create(sor_grid** out, int64_t N, const double* init, sor_dtype dt);
+int sor_create_rect(sor_grid** out, int64_t rows, int64_t cols, const double* init,
+                    sor_dtype dt);
+
+/* Multi-GPU, one process per GPU (row slabs, §8(e)): rank r of nranks owns a
+ * contiguous block of interior rows (sizes differ by <= 1),
+ * exchanges halo rows with ranks r-1 and r+1 over NCCL (NVLink) and joins the
+ * max-change with an NCCL allreduce-max.  `nccl_id` is the 128-byte
+ * ncclUniqueId from sor_nccl_unique_id() on rank 0, broadcast by the caller
+ * (e.g. torch.distributed).  `device` is the CUDA ordinal for this rank.
+ * Every rank passes the full init array.  All later calls on a dist handle
+ * are collective: every rank calls them with identical arguments.           */
+int sor_create_dist(sor_grid** out, int64_t rows, int64_t cols, const double* init,
+                    sor_dtype dt, int rank, int nranks, int device, const void* nccl_id);
+int sor_nccl_unique_id(void* out128);
+
+/* Virtual slabs on ONE GPU (test/diagnostic mode): the same slab
+ * decomposition, halo layout and kernels as sor_create_dist with `nslabs`
+ * slabs, halo rows moved by device-to-device copies instead of NCCL.        */
+int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double* init,
+                       sor_dtype dt, int nslabs);
+
+/* Select the kernel variant.  temporal_depth T (iterations per HBM pass) is
+ * used by SOR_KERNEL_TEMPORAL only, 1 <= T <= 4 (T = 1 equals FUSED).
+ * SOR_KERNEL_SMALL requires a single-slab grid that fits in shared memory.
+ * Returns SOR_E_INVAL / SOR_E_UNSUPPORTED without changing the handle.      */
+int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth);
+
+/* Run exactly `iters` >= 0 iterations with relaxation factor 0 < omega < 2
+ * (P:100).  If last_max_change != NULL it receives max|u'-u| of the last
+ * iteration (0 if iters == 0).  The grid persists across calls.             */
+int sor_iterate(sor_grid* g, double omega, int64_t iters, double* last_max_change);
+
+/* Algorithm 1: for k = 1..maxit, one iteration; if k % check_every
+ * == 0 the max-change of iteration k is computed and the call stops as soon
+ * as it is < tol (strict).  Requires 0 < omega < 2, tol > 0 finite,
+ * maxit >= 1, 1 <= check_every <= maxit.  Outputs (nullable):
+ *   iters_out      : iterations executed in THIS call (the converging one
+ *                    included; maxit if not converged);
+ *   max_change_out : the last checked max-change (fp64).
+ * Returns SOR_OK if converged, SOR_NOT_CONVERGED if maxit was reached.      */
+int sor_solve(sor_grid* g, double omega, double tol, int64_t maxit, int64_t check_every,
+              int64_t* iters_out, double* max_change_out);
+
+/* Copy the current iterate into `out` ((rows+2)*(cols+2) fp64, host or
+ * device; fp32 grids are widened exactly).  Dist: every rank must call; rank
+ * 0 receives the whole grid, other ranks' `out` may be NULL.                */
+int sor_download(sor_grid* g, double* out);
+
+/* Copy global rows [row_a, row_b) (0 <= row_a < row_b <= rows+2, ring rows
+ * included) of the current iterate into `out` ((row_b-row_a)*(cols+2) fp64,
+ * host or device).  Single-GPU and virtual handles only.                    */
+int sor_download_rows(sor_grid* g, int64_t row_a, int64_t row_b, double* out);
+
+/* Re-load the grid from `init` (same contract as sor_create), keeping the
+ * handle's allocation, kernel choice and stream.                            */
+int sor_reset(sor_grid* g, const double* init);
+
+/* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream) for
+ * all work of this handle; NULL restores the handle's own stream.           */
+int sor_set_stream(sor_grid* g, void* cuda_stream);
+
+/* CUDA-event time (ms) of the device work of the last iterate/solve call.   */
+int sor_last_elapsed_ms(const sor_grid* g, double* ms);
+
+typedef struct {
+  int64_t kernel_launches;  /* library kernels launched by the last iterate/solve call */
+  int64_t half_sweeps;      /* colour phases executed (2 per iteration) */
+  int64_t halo_exchanges;   /* halo exchange rounds (dist / virtual)                  */
+  int64_t checks;           /* convergence checks evaluated                           */
+  int64_t hbm_passes;       /* full read+write passes over the grid                    */
+  int32_t kernel;           /* active sor_kernel                                       */
+  int32_t temporal_depth;
+  int32_t nslabs;           /* slabs held by this handle (virtual) or 1               */
+  int32_t rank, nranks;
+  int64_t row_lo, row_hi;   /* owned global interior rows [row_lo, row_hi) of slab 0  */
+  int64_t pitch_elems;      /* device row pitch in elements                           */
+} sor_stats;
+int sor_get_stats(const sor_grid* g, sor_stats* out);
+
+/* Host logic shared by the dist and virtual modes (also usable without a
+ * GPU): rank p of P owns interior rows [*lo, *hi), 1-based, contiguous,
+ * sizes differ by at most 1.  Returns SOR_E_INVAL if P < 1,
+ * p outside [0,P) or rows < P.                                              */
+int sor_partition_rows(int64_t rows, int P, int p, int64_t* lo, int64_t* hi);
+
+/* Release everything owned by the handle.  NULL-safe.                       */
+void sor_destroy(sor_grid* g);
+
+/* Thread-local text for the last non-OK status on this thread.             */
+const char* sor_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOR_H */

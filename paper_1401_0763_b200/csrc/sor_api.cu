@@ -1,0 +1,916 @@
+// sor_api.cu — C ABI (include/sor.h) and host-side driver of the B200 red-black
+// SOR hot path.  Algorithm 1 of arXiv 1401.0763 [P:283-337] re-designed for
+// sm_100a: the iteration loop is enqueued on one CUDA stream, the stop test
+// runs on the device (fused into the last part of the checking launch), and
+// the host polls a pinned copy of the device state once per batch, one batch
+// behind, so the GPU never idles on a host round trip.
+//
+// Multi-GPU (§8(e)): the grid is split into row slabs [S:232-240]; after each
+// HBM pass every slab sends its first/last h rows to its neighbours (h = 1
+// per half-sweep for K1, h = 2T per T-iteration pass for K3/K4) and, on
+// checked iterations, the per-slab max is joined by an allreduce-max.  The
+// transport is NCCL over NVLink (dist mode) or device copies (virtual mode).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sor.h"
+#include "sor_kernels.cuh"
+
+using namespace sorb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Slab {
+  int64_t g_lo = 0, g_hi = 0;  // owned global interior rows [g_lo, g_hi)
+  int64_t g0 = 0;              // global row of storage row 0 (= g_lo - kRowPad)
+  int64_t nstore = 0;          // storage rows
+  void* plane[2] = {nullptr, nullptr};
+};
+
+enum class Mode { Single, Virtual, Dist };
+
+struct KernelCache {
+  int occ_blocks = 0;  // resident CTAs per SM for the wave kernel instance
+};
+
+}  // namespace
+
+struct sor_grid {
+  int64_t rows = 0, cols = 0;
+  sor_dtype dt = SOR_F64;
+  size_t esz = 8;
+  int64_t pitch = 0;  // elements
+  Mode mode = Mode::Single;
+  std::vector<Slab> slabs;
+  int cur = 0;  // plane holding the current iterate (same for all slabs)
+  int kernel = SOR_KERNEL_FUSED;
+  int tdepth = 1;
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  DevState* dstate = nullptr;
+  DevState* hstate = nullptr;  // pinned, 2 slots for one-batch-behind polling
+  double* scratch = nullptr;   // f64 staging for f32 pack/unpack and dist gather
+  size_t scratch_bytes = 0;
+  unsigned int* dflag = nullptr;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  int halo_valid = kRowPad;  // rows of the current plane's halos known up to date
+  std::vector<std::pair<int64_t, int>> pass_ends;  // (last iteration of pass, cur after it)
+  bool failed = false;
+  bool have_elapsed = false;
+  double elapsed_ms = 0.0;
+  sor_stats st{};
+};
+
+namespace {
+
+int set_error(sor_grid* g, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (g && (code == SOR_E_CUDA || code == SOR_E_NCCL)) g->failed = true;
+  return code;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return set_error(g, SOR_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NC(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                            \
+      return set_error(g, SOR_E_NCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define TRY(expr)             \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ < 0) return rc_;  \
+  } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int partition(int64_t rows, int P, int p, int64_t* lo, int64_t* hi) {
+  if (P < 1 || p < 0 || p >= P || rows < P) return SOR_E_INVAL;
+  const int64_t base = rows / P, rem = rows % P;
+  const int64_t start = 1 + p * base + std::min<int64_t>(p, rem);
+  *lo = start;
+  *hi = start + base + (p < rem ? 1 : 0);
+  return SOR_OK;
+}
+
+template <typename R>
+R* col0(void* plane) {
+  return reinterpret_cast<R*>(plane) + kColPad;
+}
+
+cudaMemcpyKind kDefault = cudaMemcpyDefault;
+
+// ------------------------------------------------------------------ layout
+// Copy global rows [ga, gb) of a full (rows+2)x(cols+2) fp64 array into plane p
+// of slab s (rounding to fp32 if needed).
+int load_rows(sor_grid* g, const Slab& s, int p, const double* init, int64_t ga, int64_t gb) {
+  if (gb <= ga) return SOR_OK;
+  const int64_t w = g->cols + 2;
+  if (g->dt == SOR_F64) {
+    CU(cudaMemcpy2DAsync(col0<double>(s.plane[p]) + (ga - s.g0) * g->pitch, g->pitch * 8,
+                         init + ga * w, w * 8, w * 8, gb - ga, kDefault, g->stream));
+    return SOR_OK;
+  }
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(g->scratch_bytes / (w * 8)));
+  for (int64_t r = ga; r < gb; r += chunk) {
+    const int64_t n = std::min(chunk, gb - r);
+    CU(cudaMemcpyAsync(g->scratch, init + r * w, n * w * 8, kDefault, g->stream));
+    dim3 grid((unsigned)std::min<int64_t>((w + 255) / 256, 1024), (unsigned)std::min<int64_t>(n, 65535));
+    narrow_rows<<<grid, 256, 0, g->stream>>>(g->scratch, w, col0<float>(s.plane[p]) + (r - s.g0) * g->pitch,
+                                             g->pitch, n, w);
+    CU(cudaGetLastError());
+  }
+  return SOR_OK;
+}
+
+// Copy global rows [ga, gb) of plane p of slab s into a full fp64 array.
+int store_rows(sor_grid* g, const Slab& s, int p, double* out, int64_t ga, int64_t gb) {
+  if (gb <= ga) return SOR_OK;
+  const int64_t w = g->cols + 2;
+  if (g->dt == SOR_F64) {
+    CU(cudaMemcpy2DAsync(out + ga * w, w * 8, col0<double>(s.plane[p]) + (ga - s.g0) * g->pitch,
+                         g->pitch * 8, w * 8, gb - ga, kDefault, g->stream));
+    return SOR_OK;
+  }
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(g->scratch_bytes / (w * 8)));
+  for (int64_t r = ga; r < gb; r += chunk) {
+    const int64_t n = std::min(chunk, gb - r);
+    dim3 grid((unsigned)std::min<int64_t>((w + 255) / 256, 1024), (unsigned)std::min<int64_t>(n, 65535));
+    widen_rows<<<grid, 256, 0, g->stream>>>(col0<float>(s.plane[p]) + (r - s.g0) * g->pitch, g->pitch,
+                                            g->scratch, w, n, w);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out + r * w, g->scratch, n * w * 8, kDefault, g->stream));
+    CU(cudaStreamSynchronize(g->stream));  // scratch is reused by the next chunk
+  }
+  return SOR_OK;
+}
+
+int check_finite(sor_grid* g, const double* init, int64_t n, bool on_device) {
+  if (!on_device) {
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(init[i])) return set_error(nullptr, SOR_E_INVAL, "init[%lld] is not finite", (long long)i);
+    return SOR_OK;
+  }
+  CU(cudaMemsetAsync(g->dflag, 0, sizeof(unsigned int), g->stream));
+  count_nonfinite<<<4 * g->nsm, 256, 0, g->stream>>>(init, n, g->dflag);
+  CU(cudaGetLastError());
+  unsigned int bad = 0;
+  CU(cudaMemcpyAsync(&bad, g->dflag, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  if (bad) return set_error(nullptr, SOR_E_INVAL, "init contains non-finite values");
+  return SOR_OK;
+}
+
+// Fill both planes of every slab from init: global rows within the slab's
+// storage window that exist in [0, rows+1] (own rows, ring, initial halos).
+int load_all(sor_grid* g, const double* init) {
+  for (auto& s : g->slabs) {
+    const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
+    CU(cudaMemsetAsync(s.plane[0], 0, bytes, g->stream));
+    const int64_t ga = std::max<int64_t>(0, s.g0);
+    const int64_t gb = std::min<int64_t>(g->rows + 2, s.g0 + s.nstore);
+    TRY(load_rows(g, s, 0, init, ga, gb));
+    CU(cudaMemcpyAsync(s.plane[1], s.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
+  }
+  g->cur = 0;
+  g->halo_valid = kRowPad;
+  CU(cudaStreamSynchronize(g->stream));
+  return SOR_OK;
+}
+
+int validate_dims(int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1)
+    return set_error(nullptr, SOR_E_INVAL, "rows and cols must be >= 1 (got %lld x %lld)",
+                     (long long)rows, (long long)cols);
+  if (cols > (int64_t)1 << 30 || rows > (int64_t)1 << 34)
+    return set_error(nullptr, SOR_E_INVAL, "grid too large");
+  return SOR_OK;
+}
+
+void free_grid(sor_grid* g) {
+  if (!g) return;
+  for (auto& s : g->slabs)
+    for (int p = 0; p < 2; ++p)
+      if (s.plane[p]) cudaFree(s.plane[p]);
+  if (g->dstate) cudaFree(g->dstate);
+  if (g->hstate) cudaFreeHost(g->hstate);
+  if (g->scratch) cudaFree(g->scratch);
+  if (g->dflag) cudaFree(g->dflag);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  for (int k = 0; k < 2; ++k)
+    if (g->poll_ev[k]) cudaEventDestroy(g->poll_ev[k]);
+  if (g->own_stream) cudaStreamDestroy(g->own_stream);
+  if (g->comm) ncclCommDestroy(g->comm);
+  delete g;
+}
+
+// Common construction.  slabs_lo_hi: owned row ranges of the slabs this
+// handle holds.
+int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, int64_t>>& spans) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  g->device = dev;
+  cudaDeviceProp prop{};
+  CU(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return set_error(g, SOR_E_CUDA, "libsor.so is built for sm_100a (B200); device %d is sm_%d%d",
+                     dev, prop.major, prop.minor);
+  g->nsm = prop.multiProcessorCount;
+  g->esz = g->dt == SOR_F64 ? 8 : 4;
+  // row: [kColPad][cols+2][>= one strip of read-ahead], multiple of 32 elements
+  g->pitch = round_up(kColPad + g->cols + 2 + kWaveCols + 16, 32);
+  CU(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  g->stream = g->own_stream;
+  CU(cudaEventCreate(&g->ev0));
+  CU(cudaEventCreate(&g->ev1));
+  for (int k = 0; k < 2; ++k) CU(cudaEventCreateWithFlags(&g->poll_ev[k], cudaEventDisableTiming));
+  CU(cudaMalloc(&g->dstate, sizeof(DevState)));
+  CU(cudaMemset(g->dstate, 0, sizeof(DevState)));
+  CU(cudaMallocHost(&g->hstate, 2 * sizeof(DevState)));
+  memset(g->hstate, 0, 2 * sizeof(DevState));
+  CU(cudaMalloc(&g->dflag, sizeof(unsigned int)));
+  g->scratch_bytes = (size_t)std::max<int64_t>(64 << 20, (g->cols + 2) * 8 * 4);
+  if (g->dt == SOR_F32 || g->mode == Mode::Dist) {
+    cudaError_t e = cudaMalloc(&g->scratch, g->scratch_bytes);
+    if (e != cudaSuccess) return set_error(g, SOR_E_NOMEM, "scratch: %s", cudaGetErrorString(e));
+  }
+  for (auto& sp : spans) {
+    Slab s;
+    s.g_lo = sp.first;
+    s.g_hi = sp.second;
+    s.g0 = s.g_lo - kRowPad;
+    s.nstore = (s.g_hi - s.g_lo) + 2 * kRowPad;
+    for (int p = 0; p < 2; ++p) {
+      cudaError_t e = cudaMalloc(&s.plane[p], (size_t)s.nstore * g->pitch * g->esz);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        g->slabs.push_back(s);
+        return set_error(nullptr, SOR_E_NOMEM, "cudaMalloc of %.3f GB plane failed: %s",
+                         (double)s.nstore * g->pitch * g->esz / 1e9, cudaGetErrorString(e));
+      }
+    }
+    g->slabs.push_back(s);
+  }
+  const bool on_dev = is_device_ptr(init);
+  TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
+  TRY(load_all(g, init));
+  g->st.nslabs = (int32_t)g->slabs.size();
+  g->st.rank = g->rank;
+  g->st.nranks = g->nranks;
+  g->st.row_lo = g->slabs[0].g_lo;
+  g->st.row_hi = g->slabs[0].g_hi;
+  g->st.pitch_elems = g->pitch;
+  g->st.kernel = g->kernel;
+  g->st.temporal_depth = g->tdepth;
+  return SOR_OK;
+}
+
+int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
+                  Mode mode, int nslabs, int rank, int nranks, int device, const void* nccl_id) {
+  if (!out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
+  *out = nullptr;
+  if (!init) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
+  if (dt != SOR_F64 && dt != SOR_F32) return set_error(nullptr, SOR_E_INVAL, "bad dtype %d", (int)dt);
+  TRY(validate_dims(rows, cols));
+  std::vector<std::pair<int64_t, int64_t>> spans;
+  if (mode == Mode::Single) {
+    spans.push_back({1, rows + 1});
+  } else if (mode == Mode::Virtual) {
+    if (nslabs < 1 || rows < 8LL * nslabs)
+      return set_error(nullptr, SOR_E_INVAL, "virtual: need 1 <= nslabs and rows >= 8*nslabs");
+    for (int p = 0; p < nslabs; ++p) {
+      int64_t lo, hi;
+      partition(rows, nslabs, p, &lo, &hi);
+      spans.push_back({lo, hi});
+    }
+  } else {
+    if (nranks < 1 || rank < 0 || rank >= nranks || rows < 8LL * nranks)
+      return set_error(nullptr, SOR_E_INVAL, "dist: need 0 <= rank < nranks and rows >= 8*nranks");
+    if (!nccl_id) return set_error(nullptr, SOR_E_INVAL, "dist: nccl_id is NULL");
+    int64_t lo, hi;
+    partition(rows, nranks, rank, &lo, &hi);
+    spans.push_back({lo, hi});
+  }
+  if (mode == Mode::Dist) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return set_error(nullptr, SOR_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return set_error(nullptr, SOR_E_CUDA, "no CUDA device available (%s); libsor has no CPU fallback",
+                     cudaGetErrorString(e));
+  }
+  sor_grid* g = new sor_grid();
+  g->rows = rows;
+  g->cols = cols;
+  g->dt = dt;
+  g->mode = mode;
+  g->rank = mode == Mode::Dist ? rank : 0;
+  g->nranks = mode == Mode::Dist ? nranks : 1;
+  if (mode == Mode::Dist) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&g->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      set_error(nullptr, SOR_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      free_grid(g);
+      return SOR_E_NCCL;
+    }
+  }
+  int rc = build(g, init, spans);
+  if (rc < 0) {
+    free_grid(g);
+    return rc;
+  }
+  *out = g;
+  return SOR_OK;
+}
+
+int usable(sor_grid* g) {
+  if (!g) return set_error(nullptr, SOR_E_INVAL, "handle is NULL");
+  if (g->failed) return set_error(nullptr, SOR_E_STATE, "handle failed earlier (CUDA/NCCL error); destroy it");
+  return SOR_OK;
+}
+
+// ------------------------------------------------------------------ halos
+// After a pass wrote plane p: each slab sends its first/last h owned rows to
+// the neighbouring slabs' halo rows of the same plane.
+int exchange(sor_grid* g, int p, int h) {
+  const size_t row_bytes = (size_t)g->pitch * g->esz;
+  if (g->mode == Mode::Virtual) {
+    const int n = (int)g->slabs.size();
+    for (int k = 0; k + 1 < n; ++k) {
+      Slab& a = g->slabs[k];
+      Slab& b = g->slabs[k + 1];
+      char* ap = (char*)a.plane[p];
+      char* bp = (char*)b.plane[p];
+      // a's last h rows -> b's top halo; b's first h rows -> a's bottom halo
+      CU(cudaMemcpyAsync(bp + (a.g_hi - h - b.g0) * row_bytes, ap + (a.g_hi - h - a.g0) * row_bytes,
+                         h * row_bytes, cudaMemcpyDeviceToDevice, g->stream));
+      CU(cudaMemcpyAsync(ap + (b.g_lo - a.g0) * row_bytes, bp + (b.g_lo - b.g0) * row_bytes,
+                         h * row_bytes, cudaMemcpyDeviceToDevice, g->stream));
+    }
+    g->st.halo_exchanges += 1;
+    return SOR_OK;
+  }
+  if (g->mode != Mode::Dist || g->nranks == 1) return SOR_OK;
+  Slab& s = g->slabs[0];
+  char* pl = (char*)s.plane[p];
+  const ncclDataType_t ty = ncclUint8;
+  const size_t n = h * row_bytes;
+  NC(ncclGroupStart());
+  if (g->rank > 0) {
+    NC(ncclSend(pl + (s.g_lo - s.g0) * row_bytes, n, ty, g->rank - 1, g->comm, g->stream));
+    NC(ncclRecv(pl + (s.g_lo - h - s.g0) * row_bytes, n, ty, g->rank - 1, g->comm, g->stream));
+  }
+  if (g->rank + 1 < g->nranks) {
+    NC(ncclSend(pl + (s.g_hi - h - s.g0) * row_bytes, n, ty, g->rank + 1, g->comm, g->stream));
+    NC(ncclRecv(pl + (s.g_hi - s.g0) * row_bytes, n, ty, g->rank + 1, g->comm, g->stream));
+  }
+  NC(ncclGroupEnd());
+  g->st.halo_exchanges += 1;
+  return SOR_OK;
+}
+
+// Join the per-slab maxima and run the stop test (multi-slab modes).
+int join_and_finalize(sor_grid* g, const IterCtl& ctl) {
+  if (g->mode == Mode::Dist && g->nranks > 1)
+    NC(ncclAllReduce(&g->dstate->maxbits, &g->dstate->maxbits, 1, ncclUint64, ncclMax, g->comm,
+                     g->stream));
+  finalize_kernel<<<1, 32, 0, g->stream>>>(ctl);
+  CU(cudaGetLastError());
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+bool single_part(const sor_grid* g) { return g->slabs.size() == 1 && g->nranks == 1; }
+
+// ------------------------------------------------------------------ K1
+template <typename R>
+int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
+  const int64_t half = (g->cols + 1) / 2;
+  const bool fused_fin = single_part(g) && ctl.check;
+  for (int color = 0; color < 2; ++color) {
+    for (auto& s : g->slabs) {
+      R* base = col0<R>(s.plane[g->cur]);
+      const int64_t nr = s.g_hi - s.g_lo;
+      dim3 grid((unsigned)((half + 255) / 256), (unsigned)std::min<int64_t>(nr, 65535));
+      IterCtl c = ctl;
+      c.finalize = (color == 1 && fused_fin) ? 1 : 0;
+      c.nparts = grid.x * grid.y;
+      if (ctl.check)
+        k1_half_sweep<R, true><<<grid, 256, 0, g->stream>>>(base, g->pitch, s.g0, g->rows, g->cols,
+                                                            s.g_lo, s.g_hi, color, w, c);
+      else
+        k1_half_sweep<R, false><<<grid, 256, 0, g->stream>>>(base, g->pitch, s.g0, g->rows,
+                                                             g->cols, s.g_lo, s.g_hi, color, w, c);
+      CU(cudaGetLastError());
+      g->st.kernel_launches += 1;
+    }
+    g->st.half_sweeps += 1;
+    TRY(exchange(g, g->cur, 1));
+  }
+  g->halo_valid = 1;
+  g->st.hbm_passes += 2;
+  if (ctl.check && !fused_fin) TRY(join_and_finalize(g, ctl));
+  return SOR_OK;
+}
+
+// ------------------------------------------------------------------ K3/K4
+template <typename R, int T, bool CHECK>
+int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  const int D = 2;
+  static int occ = 0;  // resident CTAs/SM for this instance (device-independent enough)
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, D, CHECK>, kWaveWarps * 32, 0);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[g->cur]);
+  a.dst = col0<R>(s.plane[g->cur ^ 1]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = w;
+  a.s0 = -4 * ((2 * T + 3) / 4);
+  const int64_t wout = kWaveCols - 4 * T;
+  a.nstrips = (int)((g->cols + 1 - (a.s0 + 2 * T) + wout - 1) / wout);
+  const int64_t nrows = s.g_hi - s.g_lo;
+  static double waves = -1.0;
+  if (waves < 0) {
+    const char* e = getenv("SOR_WAVE_WAVES");
+    waves = e ? atof(e) : 1.0;
+    if (!(waves > 0)) waves = 1.0;
+  }
+  const int64_t target = (int64_t)(waves * g->nsm * occ * kWaveWarps);
+  int64_t nbands = std::max<int64_t>(1, (target + a.nstrips - 1) / a.nstrips);
+  int64_t bh = std::max<int64_t>(8 * T, (nrows + nbands - 1) / nbands);
+  bh = round_up(bh, 2);
+  nbands = (nrows + bh - 1) / bh;
+  a.band_h = bh;
+  a.nbands = (int)nbands;
+  const int64_t warps = (int64_t)a.nstrips * a.nbands;
+  const unsigned blocks = (unsigned)((warps + kWaveWarps - 1) / kWaveWarps);
+  IterCtl c = ctl;
+  c.finalize = fused_fin ? 1 : 0;
+  c.nparts = blocks * kWaveWarps;
+  wave_kernel<R, T, D, CHECK><<<blocks, kWaveWarps * 32, 0, g->stream>>>(a, c);
+  CU(cudaGetLastError());
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+template <typename R, bool CHECK>
+int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool fused_fin) {
+  switch (T) {
+    case 1: return launch_wave_T<R, 1, CHECK>(g, s, w, ctl, fused_fin);
+    case 2: return launch_wave_T<R, 2, CHECK>(g, s, w, ctl, fused_fin);
+    case 3: return launch_wave_T<R, 3, CHECK>(g, s, w, ctl, fused_fin);
+    case 4: return launch_wave_T<R, 4, CHECK>(g, s, w, ctl, fused_fin);
+  }
+  return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
+}
+
+// One HBM pass of T iterations; ctl.k = index of the pass's last iteration.
+template <typename R>
+int wave_pass(sor_grid* g, int T, R w, IterCtl ctl) {
+  const bool fused_fin = single_part(g) && ctl.check;
+  if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
+  for (auto& s : g->slabs) {
+    if (ctl.check)
+      TRY((launch_wave<R, true>(g, s, T, w, ctl, fused_fin)));
+    else
+      TRY((launch_wave<R, false>(g, s, T, w, ctl, fused_fin)));
+  }
+  g->cur ^= 1;
+  g->st.half_sweeps += 2 * T;
+  g->st.hbm_passes += 1;
+  TRY(exchange(g, g->cur, 2 * T));
+  g->halo_valid = 2 * T;
+  if (ctl.check && !fused_fin) TRY(join_and_finalize(g, ctl));
+  g->pass_ends.push_back({ctl.k, g->cur});
+  return SOR_OK;
+}
+
+// ------------------------------------------------------------------ K5
+template <typename R>
+int k5_run(sor_grid* g, R w, int solve, int64_t n_iter, double tol, int64_t K, int measure_last) {
+  const Slab& s = g->slabs[0];
+  const size_t smem = (size_t)(g->rows + 2) * (g->cols + 2) * sizeof(R);
+  CU(cudaFuncSetAttribute(k5_small_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k5_small_solve<R><<<1, 1024, smem, g->stream>>>(col0<R>(s.plane[g->cur]), g->pitch, s.g0, (int)g->rows,
+                                                  (int)g->cols, w, solve, n_iter, tol, K, measure_last,
+                                                  g->dstate);
+  CU(cudaGetLastError());
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+size_t k5_limit_bytes() { return 200 * 1024; }
+
+// ------------------------------------------------------------------ drivers
+int begin_call(sor_grid* g) {
+  g->st.kernel_launches = 0;
+  g->st.half_sweeps = 0;
+  g->st.halo_exchanges = 0;
+  g->st.checks = 0;
+  g->st.hbm_passes = 0;
+  g->have_elapsed = false;
+  g->pass_ends.clear();
+  CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
+  CU(cudaEventRecord(g->ev0, g->stream));
+  return SOR_OK;
+}
+
+int end_call(sor_grid* g, DevState* out) {
+  CU(cudaEventRecord(g->ev1, g->stream));
+  CU(cudaMemcpyAsync(&g->hstate[0], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+  g->elapsed_ms = ms;
+  g->have_elapsed = true;
+  if (out) *out = g->hstate[0];
+  return SOR_OK;
+}
+
+// Enqueue iterations [k_from, k_to] (1-based within the call).  Passes of up
+// to T iterations end exactly at every iteration that must be checked.
+template <typename R>
+int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl& base,
+                  int64_t K_check, bool check_last) {
+  int64_t k = k_from;
+  while (k <= k_to) {
+    // next iteration needing a check
+    int64_t next_check = k_to + 1;
+    if (base.solve) {
+      next_check = ((k + K_check - 1) / K_check) * K_check;
+    } else if (check_last) {
+      next_check = k_to;
+    }
+    int64_t end = std::min(k_to, next_check);  // inclusive end of this block
+    if (g->kernel == SOR_KERNEL_NATURAL) {
+      for (; k <= end; ++k) {
+        IterCtl c = base;
+        c.k = k;
+        c.check = (k == next_check) ? 1 : 0;
+        TRY(k1_iteration<R>(g, w, c));
+        if (c.check) g->st.checks += 1;
+      }
+    } else {
+      const int T = g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1;
+      while (k <= end) {
+        const int64_t left = end - k + 1;
+        // remainder first so the pass containing a check ends on it
+        int t = (int)(left % T);
+        if (t == 0) t = T;
+        IterCtl c = base;
+        c.k = k + t - 1;
+        c.check = (c.k == next_check) ? 1 : 0;
+        TRY(wave_pass<R>(g, t, w, c));
+        if (c.check) g->st.checks += 1;
+        k += t;
+      }
+    }
+  }
+  return SOR_OK;
+}
+
+template <typename R>
+int iterate_impl(sor_grid* g, double omega, int64_t iters, double* last) {
+  TRY(begin_call(g));
+  const R w = (R)omega;
+  if (iters > 0) {
+    if (g->kernel == SOR_KERNEL_SMALL) {
+      TRY(k5_run<R>(g, w, 0, iters, 1.0, 1, last ? 1 : 0));
+      g->st.half_sweeps += 2 * iters;
+    } else {
+      IterCtl base{};
+      base.st = g->dstate;
+      base.maxit = iters;
+      base.tol = 0.0;
+      base.solve = 0;
+      TRY(enqueue_range<R>(g, w, 1, iters, base, 1, last != nullptr));
+    }
+  }
+  DevState hs{};
+  TRY(end_call(g, &hs));
+  if (last) *last = iters > 0 ? hs.max_change : 0.0;
+  return SOR_OK;
+}
+
+template <typename R>
+int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, int64_t* iters_out,
+               double* max_out) {
+  TRY(begin_call(g));
+  const R w = (R)omega;
+  DevState hs{};
+  if (g->kernel == SOR_KERNEL_SMALL) {
+    TRY(k5_run<R>(g, w, 1, maxit, tol, K, 0));
+    TRY(end_call(g, &hs));
+    g->st.half_sweeps = 2 * hs.iters_done;
+    g->st.checks = hs.checks;
+  } else {
+    IterCtl base{};
+    base.st = g->dstate;
+    base.maxit = maxit;
+    base.tol = tol;
+    base.solve = 1;
+    const int cur0 = g->cur;
+    // batches of whole check blocks; poll one batch behind
+    const int64_t per_batch_min = 64;
+    const int64_t blk = std::max<int64_t>(K, ((per_batch_min + K - 1) / K) * K);
+    int64_t k = 1;
+    int b = 0;
+    bool stopped = false;
+    while (k <= maxit) {
+      const int64_t k_to = std::min(maxit, k + blk - 1);
+      TRY(enqueue_range<R>(g, w, k, k_to, base, K, false));
+      CU(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                         g->stream));
+      CU(cudaEventRecord(g->poll_ev[b & 1], g->stream));
+      k = k_to + 1;
+      if (b >= 1) {
+        CU(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
+        if (g->hstate[(b - 1) & 1].stop) {
+          stopped = true;
+          break;
+        }
+      }
+      ++b;
+    }
+    (void)stopped;
+    TRY(end_call(g, &hs));
+    const int64_t done = hs.converged ? hs.conv_iter : maxit;
+    // ping-pong kernels: the plane holding X_done.  Early-exited launches
+    // wrote nothing, but the host flipped cur for every pass it enqueued.
+    if (g->kernel != SOR_KERNEL_NATURAL) {
+      int c = cur0;
+      for (auto& pe : g->pass_ends)
+        if (pe.first == done) {
+          c = pe.second;
+          break;
+        }
+      g->cur = c;
+    }
+    g->st.half_sweeps = 2 * done;
+    hs.iters_done = done;
+  }
+  if (iters_out) *iters_out = hs.converged ? hs.conv_iter : maxit;
+  if (max_out) *max_out = hs.max_change;
+  return hs.converged ? SOR_OK : SOR_NOT_CONVERGED;
+}
+
+int validate_omega(double omega) {
+  if (!(omega > 0.0 && omega < 2.0))
+    return set_error(nullptr, SOR_E_INVAL, "omega must satisfy 0 < omega < 2 (P:100), got %g", omega);
+  return SOR_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+const char* sor_last_error(void) { return g_last_error.c_str(); }
+
+int sor_partition_rows(int64_t rows, int P, int p, int64_t* lo, int64_t* hi) {
+  if (!lo || !hi) return set_error(nullptr, SOR_E_INVAL, "NULL output");
+  int rc = partition(rows, P, p, lo, hi);
+  if (rc) return set_error(nullptr, rc, "partition: need P >= 1, 0 <= p < P, rows >= P");
+  return SOR_OK;
+}
+
+int sor_create(sor_grid** out, int64_t N, const double* init, sor_dtype dt) {
+  return create_common(out, N, N, init, dt, Mode::Single, 1, 0, 1, 0, nullptr);
+}
+
+int sor_create_rect(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt) {
+  return create_common(out, rows, cols, init, dt, Mode::Single, 1, 0, 1, 0, nullptr);
+}
+
+int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
+                       int nslabs) {
+  return create_common(out, rows, cols, init, dt, Mode::Virtual, nslabs, 0, 1, 0, nullptr);
+}
+
+int sor_create_dist(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
+                    int rank, int nranks, int device, const void* nccl_id) {
+  return create_common(out, rows, cols, init, dt, Mode::Dist, 1, rank, nranks, device, nccl_id);
+}
+
+int sor_nccl_unique_id(void* out128) {
+  if (!out128) return set_error(nullptr, SOR_E_INVAL, "NULL output");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_error(nullptr, SOR_E_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(out128, &id, sizeof id);
+  return SOR_OK;
+}
+
+int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
+  TRY(usable(g));
+  switch (kernel) {
+    case SOR_KERNEL_NATURAL:
+    case SOR_KERNEL_FUSED:
+      g->kernel = kernel;
+      g->tdepth = 1;
+      break;
+    case SOR_KERNEL_TEMPORAL:
+      if (temporal_depth < 1 || temporal_depth > 4)
+        return set_error(nullptr, SOR_E_INVAL, "temporal_depth must be in [1,4], got %d", temporal_depth);
+      if (g->slabs.size() > 1 || g->nranks > 1) {
+        for (auto& s : g->slabs)
+          if (s.g_hi - s.g_lo < 2 * temporal_depth)
+            return set_error(nullptr, SOR_E_INVAL, "slab of %lld rows too thin for T=%d",
+                             (long long)(s.g_hi - s.g_lo), temporal_depth);
+      }
+      g->kernel = kernel;
+      g->tdepth = temporal_depth;
+      break;
+    case SOR_KERNEL_SMALL: {
+      if (!single_part(g))
+        return set_error(nullptr, SOR_E_UNSUPPORTED, "SOR_KERNEL_SMALL needs a single-slab grid");
+      const size_t bytes = (size_t)(g->rows + 2) * (g->cols + 2) * g->esz;
+      if (bytes > k5_limit_bytes())
+        return set_error(nullptr, SOR_E_UNSUPPORTED, "grid of %zu bytes exceeds shared memory", bytes);
+      g->kernel = kernel;
+      g->tdepth = 1;
+      break;
+    }
+    default:
+      return set_error(nullptr, SOR_E_INVAL, "unknown kernel %d", kernel);
+  }
+  g->st.kernel = g->kernel;
+  g->st.temporal_depth = g->tdepth;
+  return SOR_OK;
+}
+
+int sor_set_stream(sor_grid* g, void* cuda_stream) {
+  TRY(usable(g));
+  CU(cudaStreamSynchronize(g->stream));
+  g->stream = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
+  return SOR_OK;
+}
+
+int sor_iterate(sor_grid* g, double omega, int64_t iters, double* last_max_change) {
+  TRY(usable(g));
+  TRY(validate_omega(omega));
+  if (iters < 0) return set_error(nullptr, SOR_E_INVAL, "iters must be >= 0");
+  if (g->dt == SOR_F64) return iterate_impl<double>(g, omega, iters, last_max_change);
+  return iterate_impl<float>(g, omega, iters, last_max_change);
+}
+
+int sor_solve(sor_grid* g, double omega, double tol, int64_t maxit, int64_t check_every,
+              int64_t* iters_out, double* max_change_out) {
+  TRY(usable(g));
+  TRY(validate_omega(omega));
+  if (!(tol > 0.0) || !std::isfinite(tol)) return set_error(nullptr, SOR_E_INVAL, "tol must be finite and > 0");
+  if (maxit < 1) return set_error(nullptr, SOR_E_INVAL, "maxit must be >= 1");
+  if (check_every < 1 || check_every > maxit)
+    return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
+  if (g->dt == SOR_F64) return solve_impl<double>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
+  return solve_impl<float>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
+}
+
+int sor_download(sor_grid* g, double* out) {
+  TRY(usable(g));
+  if (g->mode != Mode::Dist || g->rank == 0) {
+    if (!out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
+  }
+  CU(cudaStreamSynchronize(g->stream));
+  if (g->mode != Mode::Dist) {
+    const int n = (int)g->slabs.size();
+    for (int k = 0; k < n; ++k) {
+      const Slab& s = g->slabs[k];
+      const int64_t ga = k == 0 ? 0 : s.g_lo;
+      const int64_t gb = k == n - 1 ? g->rows + 2 : s.g_hi;
+      TRY(store_rows(g, s, g->cur, out, ga, gb));
+    }
+    CU(cudaStreamSynchronize(g->stream));
+    return SOR_OK;
+  }
+  // dist: rank 0 gathers every slab (owned rows; first/last include the ring)
+  const Slab& s = g->slabs[0];
+  const size_t row_bytes = (size_t)g->pitch * g->esz;
+  const int64_t my_a = g->rank == 0 ? 0 : s.g_lo;
+  const int64_t my_b = g->rank == g->nranks - 1 ? g->rows + 2 : s.g_hi;
+  if (g->rank == 0) {
+    TRY(store_rows(g, s, g->cur, out, my_a, my_b));
+    for (int p = 1; p < g->nranks; ++p) {
+      int64_t lo, hi;
+      partition(g->rows, g->nranks, p, &lo, &hi);
+      const int64_t a = lo, b = p == g->nranks - 1 ? g->rows + 2 : hi;
+      // receive into a temporary slab-shaped buffer, then unpack
+      void* tmp = nullptr;
+      CU(cudaMalloc(&tmp, (size_t)(b - a) * row_bytes));
+      NC(ncclRecv(tmp, (b - a) * row_bytes, ncclUint8, p, g->comm, g->stream));
+      Slab t;
+      t.g0 = a;
+      t.plane[0] = (char*)tmp - 0;  // rows start at global row a
+      t.nstore = b - a;
+      t.plane[1] = t.plane[0];
+      int rc = store_rows(g, t, 0, out, a, b);
+      CU(cudaStreamSynchronize(g->stream));
+      cudaFree(tmp);
+      if (rc < 0) return rc;
+    }
+  } else {
+    NC(ncclSend((char*)s.plane[g->cur] + (my_a - s.g0) * row_bytes, (my_b - my_a) * row_bytes,
+                ncclUint8, 0, g->comm, g->stream));
+  }
+  CU(cudaStreamSynchronize(g->stream));
+  return SOR_OK;
+}
+
+int sor_download_rows(sor_grid* g, int64_t row_a, int64_t row_b, double* out) {
+  TRY(usable(g));
+  if (g->mode == Mode::Dist) return set_error(nullptr, SOR_E_UNSUPPORTED, "download_rows: not on dist handles");
+  if (!out || row_a < 0 || row_b > g->rows + 2 || row_a >= row_b)
+    return set_error(nullptr, SOR_E_INVAL, "download_rows: need 0 <= row_a < row_b <= rows+2 and out");
+  CU(cudaStreamSynchronize(g->stream));
+  const int n = (int)g->slabs.size();
+  const int64_t w = g->cols + 2;
+  for (int k = 0; k < n; ++k) {
+    const Slab& s = g->slabs[k];
+    const int64_t sa = std::max(row_a, k == 0 ? (int64_t)0 : s.g_lo);
+    const int64_t sb = std::min(row_b, k == n - 1 ? g->rows + 2 : s.g_hi);
+    if (sa >= sb) continue;
+    // store_rows indexes `out` by global row; shift the base accordingly
+    TRY(store_rows(g, s, g->cur, out - row_a * w, sa, sb));
+  }
+  CU(cudaStreamSynchronize(g->stream));
+  return SOR_OK;
+}
+
+int sor_reset(sor_grid* g, const double* init) {
+  TRY(usable(g));
+  if (!init) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
+  const bool on_dev = is_device_ptr(init);
+  TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
+  return load_all(g, init);
+}
+
+int sor_last_elapsed_ms(const sor_grid* g, double* ms) {
+  if (!g || !ms) return set_error(nullptr, SOR_E_INVAL, "NULL argument");
+  if (!g->have_elapsed) return set_error(nullptr, SOR_E_STATE, "no iterate/solve call timed yet");
+  *ms = g->elapsed_ms;
+  return SOR_OK;
+}
+
+int sor_get_stats(const sor_grid* g, sor_stats* out) {
+  if (!g || !out) return set_error(nullptr, SOR_E_INVAL, "NULL argument");
+  *out = g->st;
+  return SOR_OK;
+}
+
+void sor_destroy(sor_grid* g) {
+  if (!g) return;
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  free_grid(g);
+}
+
+}  // extern "C"

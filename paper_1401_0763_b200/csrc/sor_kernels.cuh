@@ -1,0 +1,467 @@
+// sor_kernels.cuh — sm_100a kernels of the red-black SOR hot path.
+//
+// Method: arXiv 1401.0763 (P:n = PAPER.md line n).  Per interior cell, Eq. 1
+// [§2.1, P:97-100] in the canonical form of include/sor.h:
+//     s = (uN+uS)+(uW+uE); a = 0.25*s; r = a - u; u' = u + w*r
+// written with __dadd_rn/__dmul_rn (__fadd_rn/__fmul_rn) so no FMA
+// contraction or reassociation can change a bit (readings #3-#4).  Colour of
+// (g, j) with g the GLOBAL row: red iff (g + j) even [P:149]; red phase first,
+// black phase reads the new reds [P:198].  Max-change [P:103, P:319-325] =
+// max |u' - u| over owned interior cells, reduced as ordered u64 bits.
+//
+// Kernels:
+//   k1_half_sweep  K1: one colour phase in place (natural layout), one thread
+//                  per cell of that colour; 2 launches per iteration.
+//   wave_kernel    K3 (T=1) / K4 (T>1): T red+black iterations per HBM pass.
+//                  One warp streams a 128-column strip down a band of rows in
+//                  registers: src row i+1 enters, stage s (half-sweep s, colour
+//                  s&1) updates row i-s, the last stage emits finished row
+//                  i-2T+1 to dst.  N/S neighbours are in the lane's own
+//                  registers, one of W/E in the lane, the other one lane away
+//                  (one shuffle per cell pair).  Strips overlap by 2T columns
+//                  and bands by 2T rows of redundant ("ghost") work so warps
+//                  never synchronise.  Out-of-place src -> dst, so the result
+//                  is bitwise that of the in-place red/black sequence
+//                  (DESIGN.md §5.2).
+//   k5_small_solve K5: whole grid in one CTA's shared memory; all iterations,
+//                  max-change and stop test in one launch.
+//   finalize_kernel  stop test after a cross-slab (virtual / NCCL) max.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sorb {
+
+constexpr int kColPad = 32;   // storage columns left of global column 0
+constexpr int kRowPad = 24;   // storage rows above/below a slab's owned rows + halo
+constexpr int kWaveWarps = 4; // warps per CTA in wave_kernel (independent warps)
+constexpr int kWaveCols = 128;  // columns per warp strip (4 per lane)
+
+struct DevState {
+  unsigned long long maxbits;  // ordered bits of max |delta| (non-negative doubles)
+  unsigned int ticket;         // finishing-part counter for the fused finalize
+  int stop;                    // solve: converged or maxit reached -> later launches exit
+  int converged;
+  int pad0;
+  long long iters_done;        // iterations finished in this call
+  long long conv_iter;
+  long long checks;
+  double max_change;           // last checked max-change
+};
+
+struct IterCtl {
+  DevState* st;         // nullptr: no max-change, no loop control
+  long long k;          // 1-based index (in this call) of the iteration this launch completes
+  long long maxit;
+  double tol;
+  int check;            // reduce max|delta| of iteration k
+  int solve;            // apply the stop test / early exit
+  int finalize;         // this launch's last part runs the stop test
+  unsigned int nparts;  // number of ticket takers (warps or CTAs) in this launch
+};
+
+// ---------------------------------------------------------------- arithmetic
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+
+// Eq. 1, BJ form, canonical order.  ns = uN+uS and we = uW+uE are formed by the
+// caller (addition is commutative, so which operand is W and which E is moot).
+template <typename R>
+__device__ __forceinline__ R sor_update(R ns, R we, R u, R w) {
+  const R s = radd(ns, we);
+  const R a = rmul(R(0.25), s);
+  const R r = rsub(a, u);
+  return radd(u, rmul(w, r));
+}
+
+// |u' - u| as ordered u64 bits; fp32 widened exactly first.
+__device__ __forceinline__ unsigned long long delta_bits(double un, double u) {
+  return (unsigned long long)__double_as_longlong(fabs(rsub(un, u)));
+}
+__device__ __forceinline__ unsigned long long delta_bits(float un, float u) {
+  return (unsigned long long)__double_as_longlong((double)fabsf(rsub(un, u)));
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = umax64(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+__device__ __forceinline__ int ld_stop(const DevState* st) {
+  return *reinterpret_cast<const volatile int*>(&st->stop);
+}
+
+// Stop test of Algorithm 1 [P:319-331] for iteration ctl.k; the max of the
+// iteration is already complete in st->maxbits.  Strict '<' (reading #7).
+__device__ __forceinline__ void finalize_iteration(DevState* st, const IterCtl& ctl) {
+  const unsigned long long bits = atomicExch(&st->maxbits, 0ull);
+  st->ticket = 0u;
+  st->iters_done = ctl.k;
+  if (ctl.check) {
+    const double m = __longlong_as_double((long long)bits);
+    st->checks += 1;
+    st->max_change = m;
+    if (ctl.solve && m < ctl.tol) {
+      st->converged = 1;
+      st->conv_iter = ctl.k;
+      st->stop = 1;
+    }
+  }
+  if (ctl.solve && ctl.k >= ctl.maxit) st->stop = 1;
+  __threadfence();
+}
+
+// One part (warp or CTA) contributes its max; the last part finalizes.
+__device__ __forceinline__ void contribute_and_maybe_finalize(const IterCtl& ctl,
+                                                              unsigned long long bits) {
+  if (bits) atomicMax(&ctl.st->maxbits, bits);
+  if (ctl.finalize) {
+    __threadfence();
+    const unsigned int t = atomicAdd(&ctl.st->ticket, 1u);
+    if (t == ctl.nparts - 1u) {
+      __threadfence();
+      finalize_iteration(ctl.st, ctl);
+    }
+  }
+}
+
+__global__ void finalize_kernel(IterCtl ctl) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (ctl.solve && ld_stop(ctl.st)) return;
+    finalize_iteration(ctl.st, ctl);
+  }
+}
+
+// ---------------------------------------------------------------- K1
+// One colour phase (updateGridRed / updateGridBlack) over owned
+// global rows [r_lo, r_hi), in place.  Code 2's stride-2 form:
+// thread t of row g updates column j0(g) + 2t, no parity branch per cell.
+template <typename R, bool CHECK>
+__global__ void __launch_bounds__(256) k1_half_sweep(R* base, long long pitch, long long g0,
+                                                     long long rows, long long cols,
+                                                     long long r_lo, long long r_hi, int color,
+                                                     R w, IterCtl ctl) {
+  if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  unsigned long long dmax = 0ull;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long g = r_lo + blockIdx.y; g < r_hi; g += gridDim.y) {
+    const long long j = ((((g + 1) & 1) == color) ? 1 : 2) + 2 * t;
+    if (j <= cols && g >= 1 && g <= rows) {
+      const R* up = base + (g - 1 - g0) * pitch;
+      R* uc = base + (g - g0) * pitch;
+      const R* dn = base + (g + 1 - g0) * pitch;
+      const R u = uc[j];
+      const R un = sor_update(radd(up[j], dn[j]), radd(uc[j - 1], uc[j + 1]), u, w);
+      if (CHECK) dmax = umax64(dmax, delta_bits(un, u));
+      uc[j] = un;
+    }
+  }
+  if (CHECK) {
+    dmax = warp_max_u64(dmax);
+    __shared__ unsigned long long wmax[8];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0ull;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = umax64(m, wmax[k]);
+      contribute_and_maybe_finalize(ctl, m);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K3 / K4
+template <typename R>
+struct WaveArgs {
+  const R* src;      // column 0 of storage row 0 (plane + kColPad)
+  R* dst;
+  long long pitch;   // elements
+  long long g0;      // global row of storage row 0
+  long long rows, cols;
+  long long r_lo, r_hi;  // owned global rows written by this launch
+  long long band_h;
+  int nstrips, nbands;
+  int s0;            // first column of strip 0 (multiple of 4)
+  R w;
+};
+
+__device__ __forceinline__ void ldg4(const double* p, double (&x)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ldg4(const float* p, float (&x)[4]) {
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg4(double* p, const double (&x)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x[0]), "d"(x[1]),
+               "d"(x[2]), "d"(x[3])
+               : "memory");
+}
+__device__ __forceinline__ void stg4(float* p, const float (&x)[4]) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(x[0]), "f"(x[1]),
+               "f"(x[2]), "f"(x[3])
+               : "memory");
+}
+
+template <typename R>
+__device__ __forceinline__ R shfl_up1(R v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+template <typename R>
+__device__ __forceinline__ R shfl_dn1(R v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// Register pipeline of one warp.  Lane columns c0..c0+3 (q = 0..3).  At a
+// step with front row i and O = i & 1, the cells of stage s (colour s&1) in
+// row i-s sit at q = O and O+2; stages keep only their own colour ("compact
+// pairs", v[0] <-> q=O, v[1] <-> q=O+2 of the step that produced them).
+template <typename R, int T, int D, bool CHECK>
+struct WavePipe {
+  static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
+  R F[3][4];                       // src rows i-1, i, i+1 (full width)
+  R C[S - 1][3][2];                // stage outputs, age 0 (newest) .. 2
+  R L[D][4];                       // prefetched src rows i+2 .. i+1+D
+  bool upd[4], own[4];
+  bool own_all;
+  unsigned long long dmax;
+
+  template <int O, int SL>
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, long long i, long long c0,
+                                       long long R0, long long R1) {
+    // shift rings, take the prefetched row i+1, prefetch row i+1+D
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      F[0][q] = F[1][q];
+      F[1][q] = F[2][q];
+      F[2][q] = L[SL][q];
+    }
+    ldg4(a.src + (i + 1 + D - a.g0) * a.pitch + c0, L[SL]);
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+      C[s][2][0] = C[s][1][0];
+      C[s][2][1] = C[s][1][1];
+      C[s][1][0] = C[s][0][0];
+      C[s][1][1] = C[s][0][1];
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const long long r = i - s;
+      const bool rowok = (r >= 1) & (r <= a.rows);
+      R n0, n1, s0, s1, w0, w1, u0, u1;
+      if (s == 0) {
+        n0 = F[0][O]; n1 = F[0][O + 2];
+        s0 = F[2][O]; s1 = F[2][O + 2];
+        w0 = F[1][1 - O]; w1 = F[1][3 - O];
+        u0 = F[1][O]; u1 = F[1][O + 2];
+      } else {
+        const int p = s > 0 ? s - 1 : 0;
+        n0 = C[p][2][0]; n1 = C[p][2][1];
+        s0 = C[p][0][0]; s1 = C[p][0][1];
+        w0 = C[p][1][0]; w1 = C[p][1][1];
+        if (s == 1) {
+          u0 = F[0][O]; u1 = F[0][O + 2];
+        } else {
+          u0 = C[(s >= 2 ? s - 2 : 0)][2][0];
+          u1 = C[(s >= 2 ? s - 2 : 0)][2][1];
+        }
+      }
+      // the W/E neighbour outside the lane: q=-1 (left lane's q=3) when O=0,
+      // q=4 (right lane's q=0) when O=1
+      const R nb = (O == 0) ? shfl_up1(w1) : shfl_dn1(w0);
+      const R mid = radd(w0, w1);
+      const R weA = (O == 0) ? radd(nb, w0) : mid;
+      const R weB = (O == 0) ? mid : radd(w1, nb);
+      R v0 = sor_update(radd(n0, s0), weA, u0, a.w);
+      R v1 = sor_update(radd(n1, s1), weB, u1, a.w);
+      v0 = (rowok && upd[O]) ? v0 : u0;
+      v1 = (rowok && upd[O + 2]) ? v1 : u1;
+      if (CHECK && s >= S - 2) {
+        if (r >= R0 && r < R1 && rowok) {
+          if (own[O]) dmax = umax64(dmax, delta_bits(v0, u0));
+          if (own[O + 2]) dmax = umax64(dmax, delta_bits(v1, u1));
+        }
+      }
+      if (s < S - 1) {
+        C[s][0][0] = v0;
+        C[s][0][1] = v1;
+      } else {
+        // finished row r: this stage's colour at q = O, O+2, the other colour
+        // from stage S-2's row r (computed one step ago at q = 1-O, 3-O)
+        if (r >= R0 && r < R1 && rowok) {
+          R out[4];
+          out[O] = v0;
+          out[O + 2] = v1;
+          out[1 - O] = C[S - 2][1][0];
+          out[3 - O] = C[S - 2][1][1];
+          R* p = a.dst + (r - a.g0) * a.pitch + c0;
+          if (own_all) {
+            stg4(p, out);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (own[q]) p[q] = out[q];
+          }
+        }
+      }
+    }
+  }
+};
+
+template <typename R, int T, int D, bool CHECK>
+__global__ void __launch_bounds__(kWaveWarps * 32) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
+  if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kWaveWarps + (threadIdx.x >> 5);
+  WavePipe<R, T, D, CHECK> P;
+  P.dmax = 0ull;
+  if (gw < a.nstrips * a.nbands) {
+    const int strip = gw % a.nstrips;
+    const int band = gw / a.nstrips;
+    const long long sw = a.s0 + (long long)strip * (kWaveCols - 4 * T);
+    const long long c0 = sw + 4 * lane;
+    const long long R0 = a.r_lo + (long long)band * a.band_h;
+    const long long R1 = min(R0 + a.band_h, a.r_hi);
+    const long long olo = max(sw + 2 * T, 1LL);
+    const long long ohi = min(sw + kWaveCols - 2 * T, a.cols + 1);
+    P.own_all = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long c = c0 + q;
+      P.upd[q] = (c >= 1) && (c <= a.cols);
+      P.own[q] = (c >= olo) && (c < ohi);
+      P.own_all = P.own_all && P.own[q];
+    }
+#pragma unroll
+    for (int s = 0; s < 2 * T - 1; ++s)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
+    // first step: stage 2T-1 reaches row R0 after 2T-1 warm-up rows; even start
+    const long long i_first = (R0 - (2 * T - 1)) & ~1LL;
+    const long long i_end_min = R1 + 2 * T - 1;  // exclusive: last step processes R1-1 at stage 2T-1
+    const long long nsteps = ((i_end_min - i_first) + D - 1) / D * D;
+    const R* sp = a.src + c0;
+    ldg4(sp + (i_first - 1 - a.g0) * a.pitch, P.F[1]);
+    ldg4(sp + (i_first - a.g0) * a.pitch, P.F[2]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) ldg4(sp + (i_first + 1 + k - a.g0) * a.pitch, P.L[k]);
+#pragma unroll 1
+    for (long long i = i_first; i < i_first + nsteps; i += D) {
+      P.template step<0, 0>(a, i, c0, R0, R1);
+      P.template step<1, 1>(a, i + 1, c0, R0, R1);
+      if (D == 4) {
+        P.template step<0, (D == 4 ? 2 : 0)>(a, i + 2, c0, R0, R1);
+        P.template step<1, (D == 4 ? 3 : 1)>(a, i + 3, c0, R0, R1);
+      }
+    }
+  }
+  if (CHECK) {
+    const unsigned long long m = warp_max_u64(P.dmax);
+    if (lane == 0) contribute_and_maybe_finalize(ctl, m);
+  }
+}
+
+// ---------------------------------------------------------------- K5
+// Whole grid (rows+2) x (cols+2) in shared memory; Algorithm 1's loop on one
+// CTA.  __syncthreads() is the phase barrier [P:314, P:317].  Used for small
+// grids (BJ configs[0]) where launch latency dominates.
+template <typename R>
+__global__ void __launch_bounds__(1024) k5_small_solve(R* base, long long pitch, long long g0,
+                                                       int rows, int cols, R w, int solve,
+                                                       long long n_iter, double tol,
+                                                       long long K, int measure_last,
+                                                       DevState* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* u = reinterpret_cast<R*>(smem_raw);
+  const int ld = cols + 2;
+  const int ncell = (rows + 2) * ld;
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+    const int i = c / ld, j = c % ld;
+    u[c] = base[(i - g0) * pitch + j];
+  }
+  __shared__ unsigned long long red[32];
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = 0;
+  __syncthreads();
+  const int half = (cols + 1) / 2;  // max cells of one colour per row
+  const int per_phase = rows * half;
+  long long k = 1;
+  for (; k <= n_iter; ++k) {
+    const int check = solve ? (k % K == 0) : (measure_last && k == n_iter);
+    unsigned long long dmax = 0ull;
+    for (int color = 0; color < 2; ++color) {
+      for (int c = threadIdx.x; c < per_phase; c += blockDim.x) {
+        const int i = 1 + c / half;
+        const int j = ((((i + 1) & 1) == color) ? 1 : 2) + 2 * (c % half);
+        if (j <= cols) {
+          R* uc = u + i * ld;
+          const R uo = uc[j];
+          const R un = sor_update(radd(uc[j - ld], uc[j + ld]), radd(uc[j - 1], uc[j + 1]), uo, w);
+          if (check) dmax = umax64(dmax, delta_bits(un, uo));
+          uc[j] = un;
+        }
+      }
+      __syncthreads();
+    }
+    if (check) {
+      dmax = warp_max_u64(dmax);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long m = 0ull;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = umax64(m, red[q]);
+        const double md = __longlong_as_double((long long)m);
+        st->checks += 1;
+        st->max_change = md;
+        if (solve && md < tol) {
+          st->converged = 1;
+          st->conv_iter = k;
+          s_stop = 1;
+        }
+      }
+      __syncthreads();
+      if (s_stop) break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    st->iters_done = k > n_iter ? n_iter : k;
+    st->stop = 1;
+  }
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+    const int i = c / ld, j = c % ld;
+    base[(i - g0) * pitch + j] = u[c];
+  }
+}
+
+// ---------------------------------------------------------------- layout
+// fp64 -> fp32 round-to-nearest (reading #17) and exact widening, row blocks.
+__global__ void narrow_rows(const double* __restrict__ src, long long src_ld, float* dst,
+                            long long dst_ld, long long nrows, long long ncols) {
+  for (long long r = blockIdx.y; r < nrows; r += gridDim.y)
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncols;
+         c += (long long)gridDim.x * blockDim.x)
+      dst[r * dst_ld + c] = __double2float_rn(src[r * src_ld + c]);
+}
+__global__ void widen_rows(const float* __restrict__ src, long long src_ld, double* dst,
+                           long long dst_ld, long long nrows, long long ncols) {
+  for (long long r = blockIdx.y; r < nrows; r += gridDim.y)
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncols;
+         c += (long long)gridDim.x * blockDim.x)
+      dst[r * dst_ld + c] = (double)src[r * src_ld + c];
+}
+// Non-finite detector for sor_create's validation of device-resident input.
+__global__ void count_nonfinite(const double* __restrict__ p, long long n, unsigned int* out) {
+  unsigned int bad = 0;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+       c += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(p[c]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(out, 1u);
+}
+
+}  // namespace sorb

@@ -1,0 +1,213 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, on the same seeded inputs (`-m gpu`, needs a B200).
+
+The bar (BASELINE.json north_star): with the canonical
+operation order and no contraction on both sides every variant is expected
+BITWISE equal to the oracle; the tests assert bitwise equality, which implies
+the stated tolerances (fp64 <= 1e-12*max|bnd|, fp32 <= 1e-5 rel, iterations
++-1).  Sizes span several warp strips (124..112 columns) and bands, with
+ragged tails, odd/even dimensions and degenerate 1-wide grids.
+"""
+import numpy as np
+import pytest
+
+import sor_inputs as SI
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [("natural", 1), ("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4)]
+SIZES = [(1, 1), (1, 9), (7, 1), (2, 2), (3, 5), (8, 8), (31, 33), (64, 64), (65, 127),
+         (130, 257), (257, 130), (300, 517)]
+
+
+@pytest.fixture(scope="module")
+def gpu(sor):
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a GPU"
+    torch.cuda.set_device(0)
+    return sor
+
+
+def _field(rows, cols, seed, dtype):
+    u = SI.random_field(rows, cols, seed=seed, lo=-50.0, hi=100.0)
+    return u
+
+
+def _oracle_iterate(orc, init, dtype, omega, iters, measure_last=False):
+    u = orc.to_storage(init, dtype)
+    rep = orc.iterate(u, omega, iters, measure_last=measure_last)
+    return u.astype(np.float64), rep
+
+
+@pytest.mark.parametrize("kernel,T", KERNELS)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("rows,cols", SIZES)
+def test_iterate_bitwise(gpu, orc, kernel, T, dtype, rows, cols):
+    init = _field(rows, cols, seed=rows * 1000 + cols, dtype=dtype)
+    iters = 7                                   # not a multiple of T: remainder passes
+    ref, rep = _oracle_iterate(orc, init, dtype, 1.7, iters, measure_last=True)
+    with gpu.Grid.create(init, dtype=dtype) as g:
+        g.set_kernel(kernel, T)
+        d = g.iterate(1.7, iters, want_delta=True)
+        out = g.download()
+    assert np.array_equal(out, ref), np.abs(out - ref).max()
+    assert d == rep.max_change
+
+
+@pytest.mark.parametrize("kernel,T", KERNELS)
+def test_iterate_many_omegas_and_continuation(gpu, orc, kernel, T):
+    init = _field(97, 250, seed=5, dtype="f64")
+    ref = init.copy()
+    with gpu.Grid.create(init) as g:
+        g.set_kernel(kernel, T)
+        for omega, n in ((0.376, 3), (1.0, 5), (1.5, 4), (1.99, 9), (1.2, 0), (1.93, 1)):
+            orc.iterate(ref, omega, n)
+            g.iterate(omega, n)
+        out = g.download()
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("kernel,T", KERNELS + [("small", 1)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_c1_solve_exact(gpu, orc, kernel, T, dtype):
+    """BJ configs[0]: iterations-to-tolerance and final grid equal to the oracle."""
+    cfg = SI.config("C1")
+    ref = orc.to_storage(cfg.init(), dtype)
+    rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, 1)
+    with gpu.Grid.create(cfg.init(), dtype=dtype) as g:
+        g.set_kernel(kernel, T)
+        r = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1)
+        out = g.download()
+    assert r.converged == rr.converged and r.iters == rr.iters
+    assert r.max_change == rr.max_change
+    assert np.array_equal(out, ref.astype(np.float64))
+
+
+@pytest.mark.parametrize("kernel,T", KERNELS)
+@pytest.mark.parametrize("K", [1, 3, 8])
+def test_solve_cadence_and_not_converged(gpu, orc, kernel, T, K):
+    init = SI.random_edges(50, 77, seed=K)
+    ref = init.copy()
+    rr = orc.solve(ref, 1.8, 1e-3, 173, check_every=K)
+    with gpu.Grid.create(init) as g:
+        g.set_kernel(kernel, T)
+        r = g.solve(1.8, 1e-3, 173, check_every=K)
+        out = g.download()
+        st = g.stats
+    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
+    assert np.array_equal(out, ref)
+    assert st["half_sweeps"] == 2 * rr.iters
+    # maxit reached
+    ref2 = init.copy()
+    rr2 = orc.solve(ref2, 1.8, 1e-30, 20, check_every=K)
+    with gpu.Grid.create(init) as g:
+        g.set_kernel(kernel, T)
+        r2 = g.solve(1.8, 1e-30, 20, check_every=K)
+        out2 = g.download()
+    assert not r2.converged and r2.iters == 20 and rr2.iters == 20
+    assert r2.max_change == rr2.max_change
+    assert np.array_equal(out2, ref2)
+
+
+def test_solve_then_continue(gpu, orc):
+    cfg = SI.config("C1")
+    ref = cfg.init()
+    orc.iterate(ref, cfg.omega, 100)
+    rr = orc.solve(ref, cfg.omega, 1e-5, 10000, 1)
+    with gpu.Grid.create(cfg.init()) as g:
+        g.iterate(cfg.omega, 100)
+        r = g.solve(cfg.omega, 1e-5, 10000, 1)
+        out = g.download()
+    assert r.iters == rr.iters and np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("nslabs", [2, 3, 4, 8])
+@pytest.mark.parametrize("kernel,T", KERNELS)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_virtual_slabs_bitwise(gpu, orc, nslabs, kernel, T, dtype):
+    """Row-slab decomposition (same kernels, halos, partition as dist mode)."""
+    init = _field(203, 150, seed=nslabs, dtype=dtype)
+    ref, rep = _oracle_iterate(orc, init, dtype, 1.9, 11, measure_last=True)
+    with gpu.Grid.create_virtual(init, nslabs, dtype=dtype) as g:
+        g.set_kernel(kernel, T)
+        d = g.iterate(1.9, 11, want_delta=True)
+        out = g.download()
+    assert np.array_equal(out, ref)
+    assert d == rep.max_change
+
+
+@pytest.mark.parametrize("nslabs", [2, 5])
+def test_virtual_slabs_solve(gpu, orc, nslabs):
+    init = SI.random_edges(120, 90, seed=11)
+    ref = init.copy()
+    rr = orc.solve(ref, 1.9, 1e-6, 5000, 1)
+    with gpu.Grid.create_virtual(init, nslabs) as g:
+        r = g.solve(1.9, 1e-6, 5000, 1)
+        out = g.download()
+    assert r.iters == rr.iters and r.max_change == rr.max_change
+    assert np.array_equal(out, ref)
+
+
+def test_device_pointers_and_reset(gpu, orc):
+    import torch
+    init = SI.random_edges(200, 333, seed=9)
+    ref = init.copy()
+    orc.iterate(ref, 1.6, 13)
+    dinit = torch.from_numpy(init).cuda()
+    dout = torch.empty_like(dinit)
+    with gpu.Grid.create(dinit) as g:
+        g.iterate(1.6, 5)
+        g.reset(dinit)                     # back to X_0
+        g.iterate(1.6, 13)
+        g.download(dout)
+        rows = g.download_rows(50, 61)
+    assert np.array_equal(dout.cpu().numpy(), ref)
+    assert np.array_equal(rows, ref[50:61])
+
+
+def test_external_stream(gpu, orc):
+    import torch
+    init = SI.random_edges(64, 300, seed=2)
+    ref = init.copy()
+    orc.iterate(ref, 1.5, 6)
+    s = torch.cuda.Stream()
+    with gpu.Grid.create(init) as g:
+        g.set_stream(s.cuda_stream)
+        g.iterate(1.5, 6)
+        g.set_stream(None)
+        out = g.download()
+    assert np.array_equal(out, ref)
+
+
+def test_invalid_calls_leave_handle_usable(gpu):
+    init = SI.north_hot(10, 10, 1.0)
+    with gpu.Grid.create(init) as g:
+        for bad in (lambda: g.iterate(2.0, 1), lambda: g.iterate(0.0, 1), lambda: g.iterate(1.0, -1),
+                    lambda: g.solve(1.5, 0.0, 10), lambda: g.solve(1.5, 1e-3, 10, 11),
+                    lambda: g.set_kernel("temporal", 5), lambda: g.set_kernel(99)):
+            with pytest.raises(gpu.SorError) as e:
+                bad()
+            assert e.value.code == gpu.SOR_E_INVAL
+        g.iterate(1.5, 2)
+    bad = init.copy()
+    bad[3, 3] = np.inf
+    with pytest.raises(gpu.SorError):
+        gpu.Grid.create(bad)
+    big = SI.north_hot(400, 400, 1.0)
+    with gpu.Grid.create(big) as g:
+        with pytest.raises(gpu.SorError) as e:
+            g.set_kernel("small")
+        assert e.value.code == gpu.SOR_E_UNSUPPORTED
+
+
+def test_zero_iterations_and_stats(gpu):
+    init = SI.north_hot(30, 30, 1.0)
+    with gpu.Grid.create(init) as g:
+        assert g.iterate(1.5, 0, want_delta=True) == 0.0
+        assert np.array_equal(g.download(), init)
+        g.set_kernel("temporal", 4)
+        g.iterate(1.5, 10)
+        st = g.stats
+        assert st["half_sweeps"] == 20 and st["hbm_passes"] == 3   # 2 + 4 + 4
+        assert st["kernel_launches"] == 3
+        assert g.elapsed_ms > 0
