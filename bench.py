@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 red-black SOR hot path (arXiv 1401.0763).
+
+Metric (BASELINE.json): GLUP/s = interior grid-point updates per second
+(rows*cols*iterations / t) and the HBM-roofline fraction of the dominant
+kernel.
+
+Default workload (N=1): BASELINE.json configs[2] "C3", the size the metric
+and the 70%-of-roofline target are quoted on: 4096x4096 interior, fp64,
+north=100, omega_opt(4096), 1000 fixed iterations then solve to
+max|du| < 1e-8 with a check every iteration, continued on the same handle.
+One step = reset the grid from the HBM-resident initial array, iterate(1000),
+solve(1e-8).  `value` counts every iteration the step executed.
+
+N>1 (torchrun, one process per GPU): the same grid split into row slabs
+(strong scaling), halos over NCCL, allreduce-max for the stop test.
+
+`--impl reference` times the CPU oracle (oracle/, plain C, threaded row-slab
+variant = Algorithm 1's P workers) on this host's cores on a bounded sample
+of the same workload; it is the reference arm for this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import sor_inputs as SI  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = SI.config(args.config, dtype=args.dtype)
+    cores = len(os.sched_getaffinity(0))
+    init = cfg.init()
+    u = oracle.to_storage(init, cfg.dtype)
+    # bounded sample per step: `sample_iters` iterations of the workload grid
+    sample_iters = args.ref_iters
+    for _ in range(args.warmup):
+        oracle.iterate(u, cfg.omega, 1, threads=cores)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.iterate(u, cfg.omega, sample_iters, threads=cores)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts)
+    glups = cfg.rows * cfg.cols * sample_iters * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": "GLUP/s", "value": glups, "unit": "GLUP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name} sample: {sample_iters} iterations of the {cfg.rows}x{cfg.cols} "
+                               f"{cfg.dtype} grid per step", "impl": "CPU oracle (oracle/sor_oracle.c, "
+                               "pthreads row slabs + barrier per phase, bitwise = serial oracle)"},
+        "cpu_baseline": {"value": glups, "unit": "GLUP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{sample_iters} iterations of {cfg.name} per step, {args.steps} steps"},
+        "e2e": {"value": glups, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, budget_s: float):
+    """Oracle (as it stands) on this host's cores, bounded to ~budget_s seconds."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    u = oracle.to_storage(cfg.init(), cfg.dtype)
+    n = 0
+    t0 = time.perf_counter()
+    chunk = 2
+    while time.perf_counter() - t0 < budget_s:
+        oracle.iterate(u, cfg.omega, chunk, threads=cores)
+        n += chunk
+    t = time.perf_counter() - t0
+    return {"value": cfg.rows * cfg.cols * n / t / 1e9, "unit": "GLUP/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} iterations of {cfg.name} ({cfg.rows}x{cfg.cols} {cfg.dtype}), "
+                      f"threaded oracle, {t:.1f} s"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--dtype", default=None)
+    ap.add_argument("--kernel", default="temporal")
+    ap.add_argument("--T", type=int, default=4)
+    ap.add_argument("--no-solve", action="store_true", help="fixed iterations only")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-iters", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.dtype is None:
+        args.dtype = "f32" if args.config == "C4F32" else "f64"
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1401_0763_b200 as P
+
+    rank, world, local = env_rank()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = SI.config(args.config, dtype=args.dtype)
+    iters_fixed = cfg.iters
+    do_solve = cfg.tol is not None and not args.no_solve
+    init_h = cfg.init()
+    init_d = torch.from_numpy(init_h).cuda()
+
+    if world > 1:
+        uid = P.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).cuda()
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+        g = P.Grid.create_dist(init_d, rank, world, local, uid, dtype=cfg.dtype)
+    else:
+        g = P.Grid.create(init_d, dtype=cfg.dtype)
+    g.set_kernel(args.kernel, args.T if args.kernel == "temporal" else 1)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step(record):
+        g.reset(init_d)
+        g.iterate(cfg.omega, iters_fixed, want_delta=True)
+        t_it = g.elapsed_ms
+        st = g.stats
+        n_iter = iters_fixed
+        n_launch = st["kernel_launches"]
+        solve_iters = 0
+        if do_solve:
+            r = g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every)
+            solve_iters = r.iters
+            n_iter += r.iters
+            n_launch += g.stats["kernel_launches"]
+        if record is not None:
+            record.append({"iters": n_iter, "solve_iters": solve_iters, "t_iterate_ms": t_it,
+                           "iterate_launches": st["kernel_launches"], "launches": n_launch,
+                           "hbm_passes": st["hbm_passes"]})
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(None)
+        flush.zero_()
+    clocks = ClockSampler(local)
+    recs = []
+    barrier()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step(recs)
+        flush.zero_()      # L2 flush between steps (256 MiB > 126 MB L2)
+    ev1.record()
+    barrier()
+    ck = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    iters_total = sum(r["iters"] for r in recs)
+    updates = cfg.rows * cfg.cols * iters_total
+    value = updates / (ms_total * 1e-3) / 1e9
+
+    # dominant kernel roofline: the fixed-iteration phase launches only the
+    # wave kernel (one launch per HBM pass of T iterations)
+    pk, pk_kind = peaks()
+    esz = 8 if cfg.dtype == "f64" else 4
+    t_launch_ms = sum(r["t_iterate_ms"] for r in recs) / sum(r["iterate_launches"] for r in recs)
+    rows_local = g.stats["row_hi"] - g.stats["row_lo"]
+    bytes_per_launch = 2 * esz * rows_local * cfg.cols          # read X_{k0} + write X_{k0+T}, once each
+    achieved = bytes_per_launch / (t_launch_ms * 1e-3) / 1e9
+    it_glups = cfg.rows * cfg.cols * iters_fixed * len(recs) / (sum(r["t_iterate_ms"] for r in recs) * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            tr = json.load(f)
+        key = f"{cfg.name}:{cfg.dtype}:{args.kernel}:{args.T}"
+        if key in tr:
+            traffic = tr[key]["dram_bytes_per_launch"]
+
+    line = {
+        "metric": "GLUP/s", "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": cfg.dtype,
+        "data": "synthetic",
+        "config": {
+            "workload": (f"{cfg.name}: {cfg.rows}x{cfg.cols} interior {cfg.dtype}, {cfg.kind}, "
+                         f"omega={cfg.omega!r}, {iters_fixed} fixed iterations"
+                         + (f" + solve to max|du|<{cfg.tol:g} (check every {cfg.check_every})" if do_solve else "")),
+            "kernel": args.kernel, "temporal_depth": args.T if args.kernel == "temporal" else 1,
+            "iterations_per_step": iters_total / len(recs),
+            "solve_iterations": recs[-1]["solve_iters"],
+            "l2": "flushed between steps (256 MiB write); grid planes 2x134 MB exceed the 126 MB L2",
+            "parallelism": f"row-slab x{world}" if world > 1 else "single GPU",
+        },
+        "fixed_phase_glups": it_glups,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "kernel": f"wave_kernel<{cfg.dtype},T={args.T if args.kernel == 'temporal' else 1}>",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_ms": t_launch_ms, "peak_kind": pk_kind,
+                     "effective_frac_16B_per_update": it_glups * 2 * esz / pk["hbm_gbs"]},
+        "gpu_launches": sum(r["launches"] for r in recs),
+        "clocks": ck,
+    }
+
+    # end-to-end through the C ABI with host buffers (H2D + D2H inside timing)
+    if not args.no_e2e and world == 1:
+        hin = torch.from_numpy(init_h).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_iters = 0
+        for _ in range(args.steps):
+            g.reset(hin)
+            g.iterate(cfg.omega, iters_fixed, want_delta=True)
+            e_iters += iters_fixed
+            if do_solve:
+                e_iters += g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every).iters
+            g.download(hout)
+        t = time.perf_counter() - t0
+        nbytes = hin.numel() * 8
+        line["e2e"] = {"value": cfg.rows * cfg.cols * e_iters / t / 1e9, "unit": "GLUP/s",
+                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
+    if rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget)
+    g.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

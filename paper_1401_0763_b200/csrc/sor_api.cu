@@ -459,10 +459,12 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
 // ------------------------------------------------------------------ K3/K4
 template <typename R, int T, bool CHECK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
-  const int D = 2;
-  static int occ = 0;  // resident CTAs/SM for this instance (device-independent enough)
+  constexpr int NST = sizeof(R) == 8 ? 8 : 12;
+  constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST>();
+  static int occ = 0;  // resident CTAs/SM for this instance
   if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, D, CHECK>, kWaveWarps * 32, 0);
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CHECK>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -497,7 +499,7 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks * kWaveWarps;
-  wave_kernel<R, T, D, CHECK><<<blocks, kWaveWarps * 32, 0, g->stream>>>(a, c);
+  wave_kernel<R, T, NST, CHECK><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
   return SOR_OK;

@@ -218,31 +218,111 @@ __device__ __forceinline__ R shfl_up1(R v) { return __shfl_up_sync(0xffffffffu, 
 template <typename R>
 __device__ __forceinline__ R shfl_dn1(R v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
+// ---- TMA bulk-copy ring (cp.async.bulk + mbarrier), one ring per warp
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void lds4(const double* p, double (&x)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+}
+__device__ __forceinline__ void lds4(const float* p, float (&x)[4]) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+}
+
+// Shared memory of wave_kernel per warp: NST row slots of kWaveCols values,
+// then NST mbarriers.
+template <typename R, int NST>
+__host__ __device__ constexpr int wave_smem_per_warp() {
+  return NST * kWaveCols * (int)sizeof(R) + NST * 8;
+}
+
 // Register pipeline of one warp.  Lane columns c0..c0+3 (q = 0..3).  At a
 // step with front row i and O = i & 1, the cells of stage s (colour s&1) in
 // row i-s sit at q = O and O+2; stages keep only their own colour ("compact
 // pairs", v[0] <-> q=O, v[1] <-> q=O+2 of the step that produced them).
-template <typename R, int T, int D, bool CHECK>
+// Source rows arrive through an NST-deep shared-memory ring filled by TMA
+// bulk copies (one 1 KB copy per row per warp, issued NST rows ahead), so
+// bytes in flight do not cost registers.
+template <typename R, int T, int NST, bool CHECK>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
   R F[3][4];                       // src rows i-1, i, i+1 (full width)
   R C[S - 1][3][2];                // stage outputs, age 0 (newest) .. 2
-  R L[D][4];                       // prefetched src rows i+2 .. i+1+D
   bool upd[4], own[4];
   bool own_all;
   unsigned long long dmax;
+  // ring
+  const R* ring;        // this warp's slots (generic pointer)
+  uint32_t ring_s;      // shared address of slot 0
+  uint32_t bar_s;       // shared address of mbarrier 0
+  const R* gsrc;        // global address of (row L0, strip column s_w)
+  long long pitch;
+  long long n_total;    // rows to stream: n = 0 .. n_total-1 (row L0 + n)
+  int lane;
 
-  template <int O, int SL>
-  __device__ __forceinline__ void step(const WaveArgs<R>& a, long long i, long long c0,
-                                       long long R0, long long R1) {
-    // shift rings, take the prefetched row i+1, prefetch row i+1+D
+  __device__ __forceinline__ void issue(long long n) {
+    // lane 0 only; slot n % NST, row L0 + n
+    const int slot = (int)(n % NST);
+    const uint32_t bar = bar_s + 8u * slot;
+    mbar_expect_tx(bar, kWaveCols * sizeof(R));
+    bulk_g2s(ring_s + slot * kWaveCols * sizeof(R), gsrc + n * pitch, kWaveCols * sizeof(R), bar);
+  }
+  __device__ __forceinline__ void consume(long long n, R (&x)[4]) {
+    const int slot = (int)(n % NST);
+    mbar_wait(bar_s + 8u * slot, (uint32_t)((n / NST) & 1));
+    lds4(ring + slot * kWaveCols + 4 * lane, x);
+    __syncwarp();
+    if (lane == 0 && n + NST < n_total) {
+      fence_proxy_async_smem();
+      issue(n + NST);
+    }
+  }
+
+  template <int O>
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, long long i, long long n,
+                                       long long c0, long long R0, long long R1) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       F[0][q] = F[1][q];
       F[1][q] = F[2][q];
-      F[2][q] = L[SL][q];
     }
-    ldg4(a.src + (i + 1 + D - a.g0) * a.pitch + c0, L[SL]);
+    consume(n, F[2]);  // row i+1
 #pragma unroll
     for (int s = 0; s < S - 1; ++s) {
       C[s][2][0] = C[s][1][0];
@@ -314,14 +394,21 @@ struct WavePipe {
   }
 };
 
-template <typename R, int T, int D, bool CHECK>
+template <typename R, int T, int NST, bool CHECK>
 __global__ void __launch_bounds__(kWaveWarps * 32) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  extern __shared__ __align__(128) unsigned char wave_smem[];
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWaveWarps + (threadIdx.x >> 5);
-  WavePipe<R, T, D, CHECK> P;
+  const int warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWaveWarps + warp;
+  WavePipe<R, T, NST, CHECK> P;
   P.dmax = 0ull;
   if (gw < a.nstrips * a.nbands) {
+    unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
+    P.ring = reinterpret_cast<const R*>(wbase);
+    P.ring_s = smem_u32(wbase);
+    P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
+    P.lane = lane;
     const int strip = gw % a.nstrips;
     const int band = gw / a.nstrips;
     const long long sw = a.s0 + (long long)strip * (kWaveCols - 4 * T);
@@ -342,23 +429,30 @@ __global__ void __launch_bounds__(kWaveWarps * 32) wave_kernel(WaveArgs<R> a, It
     for (int s = 0; s < 2 * T - 1; ++s)
 #pragma unroll
       for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
-    // first step: stage 2T-1 reaches row R0 after 2T-1 warm-up rows; even start
+    // steps i = i_first .. (even start; stage 2T-1 reaches row R0 after 2T-1
+    // warm-up rows); step i consumes src row i+1.  Rows streamed: i_first-1 ..
     const long long i_first = (R0 - (2 * T - 1)) & ~1LL;
-    const long long i_end_min = R1 + 2 * T - 1;  // exclusive: last step processes R1-1 at stage 2T-1
-    const long long nsteps = ((i_end_min - i_first) + D - 1) / D * D;
-    const R* sp = a.src + c0;
-    ldg4(sp + (i_first - 1 - a.g0) * a.pitch, P.F[1]);
-    ldg4(sp + (i_first - a.g0) * a.pitch, P.F[2]);
-#pragma unroll
-    for (int k = 0; k < D; ++k) ldg4(sp + (i_first + 1 + k - a.g0) * a.pitch, P.L[k]);
+    const long long nsteps = ((R1 + 2 * T - 1 - i_first) + 1) & ~1LL;
+    P.pitch = a.pitch;
+    P.gsrc = a.src + (i_first - 1 - a.g0) * a.pitch + sw;
+    P.n_total = nsteps + 2;
+    if (lane == 0) {
 #pragma unroll 1
-    for (long long i = i_first; i < i_first + nsteps; i += D) {
-      P.template step<0, 0>(a, i, c0, R0, R1);
-      P.template step<1, 1>(a, i + 1, c0, R0, R1);
-      if (D == 4) {
-        P.template step<0, (D == 4 ? 2 : 0)>(a, i + 2, c0, R0, R1);
-        P.template step<1, (D == 4 ? 3 : 1)>(a, i + 3, c0, R0, R1);
-      }
+      for (int k = 0; k < NST; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll 1
+      for (int k = 0; k < NST; ++k)
+        if (k < P.n_total) P.issue(k);
+    }
+    P.consume(0, P.F[1]);  // row i_first - 1
+    P.consume(1, P.F[2]);  // row i_first
+#pragma unroll 1
+    for (long long m = 0; m < nsteps; m += 2) {
+      P.template step<0>(a, i_first + m, m + 2, c0, R0, R1);
+      P.template step<1>(a, i_first + m + 1, m + 3, c0, R0, R1);
     }
   }
   if (CHECK) {
