@@ -70,7 +70,7 @@ struct sor_grid {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   int halo_valid = kRowPad;  // rows of the current plane's halos known up to date
-  std::vector<std::pair<int64_t, int>> pass_ends;  // (last iteration of pass, cur after it)
+  std::vector<std::pair<int64_t, std::pair<int, int>>> pass_ends;  // (last iteration, (cur after, T))
   bool failed = false;
   bool have_elapsed = false;
   double elapsed_ms = 0.0;
@@ -415,8 +415,8 @@ int exchange(sor_grid* g, int p, int h) {
 // Join the per-slab maxima and run the stop test (multi-slab modes).
 int join_and_finalize(sor_grid* g, const IterCtl& ctl) {
   if (g->mode == Mode::Dist && g->nranks > 1)
-    NC(ncclAllReduce(&g->dstate->maxbits, &g->dstate->maxbits, 1, ncclUint64, ncclMax, g->comm,
-                     g->stream));
+    NC(ncclAllReduce(&g->dstate->maxbits[0][0], &g->dstate->maxbits[0][0], kMaxT * 16, ncclUint64, ncclMax,
+                     g->comm, g->stream));
   finalize_kernel<<<1, 32, 0, g->stream>>>(ctl);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
@@ -429,7 +429,7 @@ bool single_part(const sor_grid* g) { return g->slabs.size() == 1 && g->nranks =
 template <typename R>
 int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
   const int64_t half = (g->cols + 1) / 2;
-  const bool fused_fin = single_part(g) && ctl.check;
+  const bool fused_fin = single_part(g) && ctl.ck != 0;
   for (int color = 0; color < 2; ++color) {
     for (auto& s : g->slabs) {
       R* base = col0<R>(s.plane[g->cur]);
@@ -438,7 +438,7 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
       IterCtl c = ctl;
       c.finalize = (color == 1 && fused_fin) ? 1 : 0;
       c.nparts = grid.x * grid.y;
-      if (ctl.check)
+      if (ctl.ck)
         k1_half_sweep<R, true><<<grid, 256, 0, g->stream>>>(base, g->pitch, s.g0, g->rows, g->cols,
                                                             s.g_lo, s.g_hi, color, w, c);
       else
@@ -452,19 +452,22 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
   }
   g->halo_valid = 1;
   g->st.hbm_passes += 2;
-  if (ctl.check && !fused_fin) TRY(join_and_finalize(g, ctl));
+  if (ctl.ck && !fused_fin) TRY(join_and_finalize(g, ctl));
   return SOR_OK;
 }
 
 // ------------------------------------------------------------------ K3/K4
-template <typename R, int T, bool CHECK>
+template <typename R>
+constexpr int wave_nst() { return sizeof(R) == 8 ? 8 : 12; }
+
+template <typename R, int T, int CK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
-  constexpr int NST = sizeof(R) == 8 ? 8 : 12;
+  constexpr int NST = wave_nst<R>();
   constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST>();
   static int occ = 0;  // resident CTAs/SM for this instance
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CHECK>, kWaveWarps * 32, smem);
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -481,59 +484,86 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
   const int64_t wout = kWaveCols - 4 * T;
   a.nstrips = (int)((g->cols + 1 - (a.s0 + 2 * T) + wout - 1) / wout);
   const int64_t nrows = s.g_hi - s.g_lo;
+  // Tiles.  Short bands waste 4T-2 ghost rows each, one partial extra wave
+  // doubles the tail, and in a single long wave the slowest warp sets the
+  // time.  So: exactly one wave when that gives bands <= kOneWaveMaxH rows,
+  // otherwise ~8 waves of bands >= kMinH rows (dynamic load balance).
   static double waves = -1.0;
+  static int64_t min_h = 0;
   if (waves < 0) {
     const char* e = getenv("SOR_WAVE_WAVES");
-    waves = e ? atof(e) : 1.0;
-    if (!(waves > 0)) waves = 1.0;
+    waves = e ? atof(e) : 0.0;  // 0 = automatic
+    const char* h = getenv("SOR_WAVE_MIN_BAND");
+    min_h = h ? atoll(h) : 0;
   }
-  const int64_t target = (int64_t)(waves * g->nsm * occ * kWaveWarps);
-  int64_t nbands = std::max<int64_t>(1, (target + a.nstrips - 1) / a.nstrips);
-  int64_t bh = std::max<int64_t>(8 * T, (nrows + nbands - 1) / nbands);
-  bh = round_up(bh, 2);
-  nbands = (nrows + bh - 1) / bh;
+  const int64_t slots = (int64_t)g->nsm * occ * kWaveWarps;
+  auto fit = [](int64_t bh, int T_) {  // even, and bh + 4T - 2 steps a multiple of 6
+    while ((bh & 1) || (bh + 4 * T_ - 2) % 6) ++bh;
+    return bh;
+  };
+  int64_t bh;
+  if (waves > 0) {
+    const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / a.nstrips);
+    bh = std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb);
+  } else {
+    const int64_t nb1 = std::max<int64_t>(1, slots / a.nstrips);  // bands in one wave
+    int64_t bh1 = fit((nrows + nb1 - 1) / nb1, T);
+    while (a.nstrips * ((nrows + bh1 - 1) / bh1) > slots) bh1 = fit(bh1 + 1, T);
+    const int64_t kOneWaveMaxH = 512, kMinH = min_h > 0 ? min_h : 256;
+    if (bh1 <= kOneWaveMaxH) {
+      bh = bh1;
+    } else {
+      const int64_t nb8 = std::max<int64_t>(1, 8 * slots / a.nstrips);
+      bh = std::max<int64_t>(kMinH, (nrows + nb8 - 1) / nb8);
+    }
+  }
+  bh = fit(bh, T);
+  int64_t nbands = (nrows + bh - 1) / bh;
   a.band_h = bh;
   a.nbands = (int)nbands;
   const int64_t warps = (int64_t)a.nstrips * a.nbands;
   const unsigned blocks = (unsigned)((warps + kWaveWarps - 1) / kWaveWarps);
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
-  c.nparts = blocks * kWaveWarps;
-  wave_kernel<R, T, NST, CHECK><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
+  c.nparts = blocks;
+  wave_kernel<R, T, NST, CK><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
 
-template <typename R, bool CHECK>
+template <typename R, int CK>
 int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool fused_fin) {
   switch (T) {
-    case 1: return launch_wave_T<R, 1, CHECK>(g, s, w, ctl, fused_fin);
-    case 2: return launch_wave_T<R, 2, CHECK>(g, s, w, ctl, fused_fin);
-    case 3: return launch_wave_T<R, 3, CHECK>(g, s, w, ctl, fused_fin);
-    case 4: return launch_wave_T<R, 4, CHECK>(g, s, w, ctl, fused_fin);
+    case 1: return launch_wave_T<R, 1, CK>(g, s, w, ctl, fused_fin);
+    case 2: return launch_wave_T<R, 2, CK>(g, s, w, ctl, fused_fin);
+    case 3: return launch_wave_T<R, 3, CK>(g, s, w, ctl, fused_fin);
+    case 4: return launch_wave_T<R, 4, CK>(g, s, w, ctl, fused_fin);
   }
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
 }
 
-// One HBM pass of T iterations; ctl.k = index of the pass's last iteration.
+// One HBM pass of ctl.T iterations ending at iteration ctl.k_last.
 template <typename R>
-int wave_pass(sor_grid* g, int T, R w, IterCtl ctl) {
-  const bool fused_fin = single_part(g) && ctl.check;
+int wave_pass(sor_grid* g, R w, IterCtl ctl) {
+  const int T = ctl.T;
+  const bool fused_fin = single_part(g) && ctl.ck != 0;
   if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
   for (auto& s : g->slabs) {
-    if (ctl.check)
-      TRY((launch_wave<R, true>(g, s, T, w, ctl, fused_fin)));
+    if (ctl.ck == 2)
+      TRY((launch_wave<R, 2>(g, s, T, w, ctl, fused_fin)));
+    else if (ctl.ck == 1)
+      TRY((launch_wave<R, 1>(g, s, T, w, ctl, fused_fin)));
     else
-      TRY((launch_wave<R, false>(g, s, T, w, ctl, fused_fin)));
+      TRY((launch_wave<R, 0>(g, s, T, w, ctl, fused_fin)));
   }
   g->cur ^= 1;
   g->st.half_sweeps += 2 * T;
   g->st.hbm_passes += 1;
   TRY(exchange(g, g->cur, 2 * T));
   g->halo_valid = 2 * T;
-  if (ctl.check && !fused_fin) TRY(join_and_finalize(g, ctl));
-  g->pass_ends.push_back({ctl.k, g->cur});
+  if (ctl.ck && !fused_fin) TRY(join_and_finalize(g, ctl));
+  g->pass_ends.push_back({ctl.k_last, {g->cur, T}});
   return SOR_OK;
 }
 
@@ -579,43 +609,49 @@ int end_call(sor_grid* g, DevState* out) {
   return SOR_OK;
 }
 
-// Enqueue iterations [k_from, k_to] (1-based within the call).  Passes of up
-// to T iterations end exactly at every iteration that must be checked.
+int depth_of(const sor_grid* g) { return g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1; }
+
+// Enqueue iterations [k_from, k_to] (1-based within the call).
+//  - iterate (base.solve == 0): passes of up to T; the last one reports its
+//    last iteration's max-change if check_last.
+//  - solve with check_every == 1 and T > 1: passes of T, each reporting the
+//    max-change of every iteration it contains (ck = 2).
+//  - otherwise: passes end exactly at every checked iteration (ck = 1 there).
 template <typename R>
-int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl& base,
-                  int64_t K_check, bool check_last) {
+int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl& base, bool check_last) {
+  const int64_t K = base.K;
+  const int T = depth_of(g);
   int64_t k = k_from;
-  while (k <= k_to) {
-    // next iteration needing a check
-    int64_t next_check = k_to + 1;
-    if (base.solve) {
-      next_check = ((k + K_check - 1) / K_check) * K_check;
-    } else if (check_last) {
-      next_check = k_to;
+  if (g->kernel == SOR_KERNEL_NATURAL) {
+    for (; k <= k_to; ++k) {
+      IterCtl c = base;
+      c.k_last = k;
+      c.T = 1;
+      c.ck = base.solve ? (k % K == 0) : (check_last && k == k_to);
+      TRY(k1_iteration<R>(g, w, c));
+      if (c.ck) g->st.checks += 1;
     }
-    int64_t end = std::min(k_to, next_check);  // inclusive end of this block
-    if (g->kernel == SOR_KERNEL_NATURAL) {
-      for (; k <= end; ++k) {
-        IterCtl c = base;
-        c.k = k;
-        c.check = (k == next_check) ? 1 : 0;
-        TRY(k1_iteration<R>(g, w, c));
-        if (c.check) g->st.checks += 1;
-      }
-    } else {
-      const int T = g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1;
-      while (k <= end) {
-        const int64_t left = end - k + 1;
-        // remainder first so the pass containing a check ends on it
-        int t = (int)(left % T);
-        if (t == 0) t = T;
-        IterCtl c = base;
-        c.k = k + t - 1;
-        c.check = (c.k == next_check) ? 1 : 0;
-        TRY(wave_pass<R>(g, t, w, c));
-        if (c.check) g->st.checks += 1;
-        k += t;
-      }
+    return SOR_OK;
+  }
+  const bool every = base.solve && K == 1 && T > 1;
+  while (k <= k_to) {
+    int64_t next_check = k_to + 1;
+    if (base.solve && !every)
+      next_check = ((k + K - 1) / K) * K;
+    else if (!base.solve && check_last)
+      next_check = k_to;
+    const int64_t end = std::min(k_to, next_check);  // inclusive end of this block
+    while (k <= end) {
+      const int64_t left = end - k + 1;
+      int t = (int)(left % T);  // remainder first, so a block ends on a full pass
+      if (t == 0) t = T;
+      IterCtl c = base;
+      c.k_last = k + t - 1;
+      c.T = t;
+      c.ck = every ? 2 : (c.k_last == next_check ? 1 : 0);
+      TRY(wave_pass<R>(g, w, c));
+      if (c.ck) g->st.checks += every ? t : 1;
+      k += t;
     }
   }
   return SOR_OK;
@@ -633,9 +669,10 @@ int iterate_impl(sor_grid* g, double omega, int64_t iters, double* last) {
       IterCtl base{};
       base.st = g->dstate;
       base.maxit = iters;
+      base.K = 1;
       base.tol = 0.0;
       base.solve = 0;
-      TRY(enqueue_range<R>(g, w, 1, iters, base, 1, last != nullptr));
+      TRY(enqueue_range<R>(g, w, 1, iters, base, last != nullptr));
     }
   }
   DevState hs{};
@@ -659,43 +696,63 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     IterCtl base{};
     base.st = g->dstate;
     base.maxit = maxit;
+    base.K = K;
     base.tol = tol;
     base.solve = 1;
     const int cur0 = g->cur;
-    // batches of whole check blocks; poll one batch behind
-    const int64_t per_batch_min = 64;
-    const int64_t blk = std::max<int64_t>(K, ((per_batch_min + K - 1) / K) * K);
+    // batches of whole check blocks (and whole passes); poll one batch behind
+    const int64_t unit = std::max<int64_t>(K, depth_of(g));
+    const int64_t blk = std::max<int64_t>(unit, (int64_t)((64 + unit - 1) / unit) * unit);
     int64_t k = 1;
     int b = 0;
-    bool stopped = false;
     while (k <= maxit) {
       const int64_t k_to = std::min(maxit, k + blk - 1);
-      TRY(enqueue_range<R>(g, w, k, k_to, base, K, false));
+      TRY(enqueue_range<R>(g, w, k, k_to, base, false));
       CU(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
                          g->stream));
       CU(cudaEventRecord(g->poll_ev[b & 1], g->stream));
       k = k_to + 1;
       if (b >= 1) {
         CU(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
-        if (g->hstate[(b - 1) & 1].stop) {
-          stopped = true;
-          break;
-        }
+        if (g->hstate[(b - 1) & 1].stop) break;
       }
       ++b;
     }
-    (void)stopped;
     TRY(end_call(g, &hs));
     const int64_t done = hs.converged ? hs.conv_iter : maxit;
-    // ping-pong kernels: the plane holding X_done.  Early-exited launches
-    // wrote nothing, but the host flipped cur for every pass it enqueued.
+    // Which plane holds X_done.  Early-exited launches wrote nothing, but the
+    // host flipped cur for every pass it enqueued.  If the converging
+    // iteration sits inside a T-deep pass (ck = 2), X_done never reached HBM:
+    // re-run the first conv_t+1 iterations of that pass from its source
+    // plane, which no later (early-exited) pass has overwritten.
     if (g->kernel != SOR_KERNEL_NATURAL) {
       int c = cur0;
-      for (auto& pe : g->pass_ends)
-        if (pe.first == done) {
-          c = pe.second;
+      for (size_t q = 0; q < g->pass_ends.size(); ++q) {
+        const auto& pe = g->pass_ends[q];
+        const int64_t k_end = pe.first;
+        const int tp = pe.second.second;
+        if (done <= k_end && done > k_end - tp) {
+          c = pe.second.first;
+          if (done != k_end) {
+            g->cur = c ^ 1;  // the pass's source plane
+            IterCtl r{};
+            r.st = nullptr;
+            r.k_last = done;
+            r.T = (int)(done - (k_end - tp));
+            r.ck = 0;
+            r.solve = 0;
+            const auto saved = g->pass_ends;
+            const auto saved_st = g->st;
+            TRY(wave_pass<R>(g, w, r));
+            g->pass_ends = saved;
+            g->st = saved_st;
+            g->st.kernel_launches += (int64_t)g->slabs.size();
+            CU(cudaStreamSynchronize(g->stream));
+            c = g->cur;
+          }
           break;
         }
+      }
       g->cur = c;
     }
     g->st.half_sweeps = 2 * done;

@@ -38,24 +38,31 @@ constexpr int kRowPad = 24;   // storage rows above/below a slab's owned rows + 
 constexpr int kWaveWarps = 4; // warps per CTA in wave_kernel (independent warps)
 constexpr int kWaveCols = 128;  // columns per warp strip (4 per lane)
 
+constexpr int kMaxT = 4;      // max temporal depth (iterations per HBM pass)
+
 struct DevState {
-  unsigned long long maxbits;  // ordered bits of max |delta| (non-negative doubles)
+  // ordered bits of max |delta| per iteration of a pass; one 128-B line each
+  // so the per-CTA atomics of different slots hit different L2 slices
+  unsigned long long maxbits[kMaxT][16];
   unsigned int ticket;         // finishing-part counter for the fused finalize
   int stop;                    // solve: converged or maxit reached -> later launches exit
   int converged;
-  int pad0;
+  int conv_t;                  // index within its pass of the converging iteration
   long long iters_done;        // iterations finished in this call
   long long conv_iter;
   long long checks;
   double max_change;           // last checked max-change
 };
 
+// Loop control of one launch (a pass of `T` iterations ending at k_last).
 struct IterCtl {
   DevState* st;         // nullptr: no max-change, no loop control
-  long long k;          // 1-based index (in this call) of the iteration this launch completes
+  long long k_last;     // 1-based index (in this call) of the pass's last iteration
   long long maxit;
+  long long K;          // check_every (solve)
   double tol;
-  int check;            // reduce max|delta| of iteration k
+  int T;                // iterations in this pass
+  int ck;               // 0: no max-change; 1: of iteration k_last; 2: of every iteration
   int solve;            // apply the stop test / early exit
   int finalize;         // this launch's last part runs the stop test
   unsigned int nparts;  // number of ticket takers (warps or CTAs) in this launch
@@ -99,36 +106,44 @@ __device__ __forceinline__ int ld_stop(const DevState* st) {
   return *reinterpret_cast<const volatile int*>(&st->stop);
 }
 
-// Stop test of Algorithm 1 [P:319-331] for iteration ctl.k; the max of the
-// iteration is already complete in st->maxbits.  Strict '<' (reading #7).
-__device__ __forceinline__ void finalize_iteration(DevState* st, const IterCtl& ctl) {
-  const unsigned long long bits = atomicExch(&st->maxbits, 0ull);
+// Stop test of Algorithm 1 [P:319-331] for the iterations of one pass; their
+// maxima are complete in st->maxbits[].  Strict '<' (reading #7).
+__device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) {
+  const long long k0 = ctl.k_last - (ctl.T - 1);
   st->ticket = 0u;
-  st->iters_done = ctl.k;
-  if (ctl.check) {
-    const double m = __longlong_as_double((long long)bits);
+  for (int t = 0; t < ctl.T; ++t) {
+    const long long k = k0 + t;
+    const int slot = ctl.ck == 2 ? t : 0;
+    const bool checked = ctl.ck == 2 ? (!ctl.solve || k % ctl.K == 0) : (t == ctl.T - 1);
+    if (!checked) continue;
+    const double m = __longlong_as_double((long long)st->maxbits[slot][0]);
     st->checks += 1;
     st->max_change = m;
+    st->iters_done = k;
     if (ctl.solve && m < ctl.tol) {
       st->converged = 1;
-      st->conv_iter = ctl.k;
+      st->conv_iter = k;
+      st->conv_t = t;
       st->stop = 1;
+      break;
     }
   }
-  if (ctl.solve && ctl.k >= ctl.maxit) st->stop = 1;
+  for (int t = 0; t < kMaxT; ++t) st->maxbits[t][0] = 0ull;
+  if (ctl.solve && ctl.k_last >= ctl.maxit) st->stop = 1;
   __threadfence();
 }
 
-// One part (warp or CTA) contributes its max; the last part finalizes.
-__device__ __forceinline__ void contribute_and_maybe_finalize(const IterCtl& ctl,
-                                                              unsigned long long bits) {
-  if (bits) atomicMax(&ctl.st->maxbits, bits);
+// One part (warp or CTA) contributes its maxima; the last part finalizes.
+__device__ __forceinline__ void contribute(const IterCtl& ctl, int slot, unsigned long long bits) {
+  if (bits) atomicMax(&ctl.st->maxbits[slot][0], bits);
+}
+__device__ __forceinline__ void maybe_finalize(const IterCtl& ctl) {
   if (ctl.finalize) {
     __threadfence();
     const unsigned int t = atomicAdd(&ctl.st->ticket, 1u);
     if (t == ctl.nparts - 1u) {
       __threadfence();
-      finalize_iteration(ctl.st, ctl);
+      finalize_pass(ctl.st, ctl);
     }
   }
 }
@@ -136,7 +151,7 @@ __device__ __forceinline__ void contribute_and_maybe_finalize(const IterCtl& ctl
 __global__ void finalize_kernel(IterCtl ctl) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     if (ctl.solve && ld_stop(ctl.st)) return;
-    finalize_iteration(ctl.st, ctl);
+    finalize_pass(ctl.st, ctl);
   }
 }
 
@@ -172,7 +187,8 @@ __global__ void __launch_bounds__(256) k1_half_sweep(R* base, long long pitch, l
     if (threadIdx.x == 0) {
       unsigned long long m = 0ull;
       for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = umax64(m, wmax[k]);
-      contribute_and_maybe_finalize(ctl, m);
+      contribute(ctl, 0, m);
+      maybe_finalize(ctl);
     }
   }
 }
@@ -213,10 +229,28 @@ __device__ __forceinline__ void stg4(float* p, const float (&x)[4]) {
                : "memory");
 }
 
-template <typename R>
-__device__ __forceinline__ R shfl_up1(R v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-template <typename R>
-__device__ __forceinline__ R shfl_dn1(R v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+// Lane shuffles by one without the convergence check __shfl_*_sync inserts
+// (the warp is converged by construction at every call site).
+__device__ __forceinline__ double shfl_up1(double v) {
+  int lo = __double2loint(v), hi = __double2hiint(v);
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;" : "+r"(lo));
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;" : "+r"(hi));
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ double shfl_dn1(double v) {
+  int lo = __double2loint(v), hi = __double2hiint(v);
+  asm volatile("shfl.sync.down.b32 %0, %0, 1, 31, -1;" : "+r"(lo));
+  asm volatile("shfl.sync.down.b32 %0, %0, 1, 31, -1;" : "+r"(hi));
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ float shfl_up1(float v) {
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;" : "+f"(v));
+  return v;
+}
+__device__ __forceinline__ float shfl_dn1(float v) {
+  asm volatile("shfl.sync.down.b32 %0, %0, 1, 31, -1;" : "+f"(v));
+  return v;
+}
 
 // ---- TMA bulk-copy ring (cp.async.bulk + mbarrier), one ring per warp
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -272,39 +306,49 @@ __host__ __device__ constexpr int wave_smem_per_warp() {
   return NST * kWaveCols * (int)sizeof(R) + NST * 8;
 }
 
-// Register pipeline of one warp.  Lane columns c0..c0+3 (q = 0..3).  At a
-// step with front row i and O = i & 1, the cells of stage s (colour s&1) in
-// row i-s sit at q = O and O+2; stages keep only their own colour ("compact
-// pairs", v[0] <-> q=O, v[1] <-> q=O+2 of the step that produced them).
-// Source rows arrive through an NST-deep shared-memory ring filled by TMA
-// bulk copies (one 1 KB copy per row per warp, issued NST rows ahead), so
-// bytes in flight do not cost registers.
-template <typename R, int T, int NST, bool CHECK>
+// Register pipeline of one warp.
+//
+// Lane columns c0..c0+3 (q = 0..3), c0 = s_w + 4*lane.  Step m has front row
+// i = i_first + m; it consumes source row i+1 and stage s (half-sweep s of the
+// pass, colour s&1) updates row i-s.  With O = i & 1 (= m & 1), the cells of
+// stage s in row i-s sit at q = O and O+2; a stage keeps only its own colour
+// ("compact pair" v[0] <-> q=O, v[1] <-> q=O+2 of the step that made it).
+// Rows are held in 3-slot rings indexed by (step mod 3), so with the loop
+// unrolled 6 ways (parity x ring phase) every register index is static and
+// no value is ever moved.  Source rows arrive through an NST-deep shared
+// ring filled by TMA bulk copies issued NST rows ahead.
+//
+// CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each.
+// MASK: false for warps whose rows and columns are all interior cells (no
+// Dirichlet/padding cell to keep fixed).  Ownership (which computed cells
+// are valid and written: the strip minus its 2T ghost columns on each side,
+// the band's rows) applies to every warp.
+template <typename R, int T, int NST, int CK, bool MASK>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
-  R F[3][4];                       // src rows i-1, i, i+1 (full width)
-  R C[S - 1][3][2];                // stage outputs, age 0 (newest) .. 2
+  static constexpr int NSLOT = CK == 2 ? T : 1;
+  R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3
+  R C[S - 1][3][2];           // stage outputs, slot = step % 3
+  unsigned long long dmax[NSLOT];
   bool upd[4], own[4];
   bool own_all;
-  unsigned long long dmax;
+  int rows, R0, R1;
   // ring
-  const R* ring;        // this warp's slots (generic pointer)
-  uint32_t ring_s;      // shared address of slot 0
-  uint32_t bar_s;       // shared address of mbarrier 0
-  const R* gsrc;        // global address of (row L0, strip column s_w)
+  const R* ring;
+  uint32_t ring_s, bar_s;
+  const R* gsrc;              // global address of (row i_first-1, column s_w)
   long long pitch;
-  long long n_total;    // rows to stream: n = 0 .. n_total-1 (row L0 + n)
+  int n_total;
   int lane;
 
-  __device__ __forceinline__ void issue(long long n) {
-    // lane 0 only; slot n % NST, row L0 + n
-    const int slot = (int)(n % NST);
+  __device__ __forceinline__ void issue(int n) {  // lane 0: row i_first-1+n -> slot n % NST
+    const int slot = n % NST;
     const uint32_t bar = bar_s + 8u * slot;
     mbar_expect_tx(bar, kWaveCols * sizeof(R));
-    bulk_g2s(ring_s + slot * kWaveCols * sizeof(R), gsrc + n * pitch, kWaveCols * sizeof(R), bar);
+    bulk_g2s(ring_s + slot * kWaveCols * sizeof(R), gsrc + (long long)n * pitch, kWaveCols * sizeof(R), bar);
   }
-  __device__ __forceinline__ void consume(long long n, R (&x)[4]) {
-    const int slot = (int)(n % NST);
+  __device__ __forceinline__ void consume(int n, R (&x)[4]) {
+    const int slot = n % NST;
     mbar_wait(bar_s + 8u * slot, (uint32_t)((n / NST) & 1));
     lds4(ring + slot * kWaveCols + 4 * lane, x);
     __syncwarp();
@@ -314,45 +358,35 @@ struct WavePipe {
     }
   }
 
-  template <int O>
-  __device__ __forceinline__ void step(const WaveArgs<R>& a, long long i, long long n,
-                                       long long c0, long long R0, long long R1) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      F[0][q] = F[1][q];
-      F[1][q] = F[2][q];
-    }
-    consume(n, F[2]);  // row i+1
-#pragma unroll
-    for (int s = 0; s < S - 1; ++s) {
-      C[s][2][0] = C[s][1][0];
-      C[s][2][1] = C[s][1][1];
-      C[s][1][0] = C[s][0][0];
-      C[s][1][1] = C[s][0][1];
-    }
+  template <int M6>
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, int m, long long c0) {
+    constexpr int O = M6 & 1;
+    constexpr int PH = M6 % 3;          // slot of age 0 (this step)
+    constexpr int P1 = (PH + 2) % 3;    // age 1
+    constexpr int P2 = (PH + 1) % 3;    // age 2
+    consume(m + 2, F[P1]);              // source row i+1 (slot (m+2)%3)
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const long long r = i - s;
-      const bool rowok = (r >= 1) & (r <= a.rows);
+      const int r = i - s;
       R n0, n1, s0, s1, w0, w1, u0, u1;
       if (s == 0) {
-        n0 = F[0][O]; n1 = F[0][O + 2];
-        s0 = F[2][O]; s1 = F[2][O + 2];
-        w0 = F[1][1 - O]; w1 = F[1][3 - O];
-        u0 = F[1][O]; u1 = F[1][O + 2];
+        n0 = F[PH][O]; n1 = F[PH][O + 2];          // row i-1
+        s0 = F[P1][O]; s1 = F[P1][O + 2];          // row i+1
+        w0 = F[P2][1 - O]; w1 = F[P2][3 - O];      // row i, other colour
+        u0 = F[P2][O]; u1 = F[P2][O + 2];          // row i, self
       } else {
         const int p = s > 0 ? s - 1 : 0;
-        n0 = C[p][2][0]; n1 = C[p][2][1];
-        s0 = C[p][0][0]; s1 = C[p][0][1];
-        w0 = C[p][1][0]; w1 = C[p][1][1];
+        n0 = C[p][P2][0]; n1 = C[p][P2][1];        // row r-1
+        s0 = C[p][PH][0]; s1 = C[p][PH][1];        // row r+1
+        w0 = C[p][P1][0]; w1 = C[p][P1][1];        // row r
         if (s == 1) {
-          u0 = F[0][O]; u1 = F[0][O + 2];
+          u0 = F[PH][O]; u1 = F[PH][O + 2];        // source row i-1
         } else {
-          u0 = C[(s >= 2 ? s - 2 : 0)][2][0];
-          u1 = C[(s >= 2 ? s - 2 : 0)][2][1];
+          const int pp = s >= 2 ? s - 2 : 0;
+          u0 = C[pp][P2][0]; u1 = C[pp][P2][1];
         }
       }
-      // the W/E neighbour outside the lane: q=-1 (left lane's q=3) when O=0,
+      // W/E neighbour outside the lane: q=-1 (left lane's q=3) when O=0,
       // q=4 (right lane's q=0) when O=1
       const R nb = (O == 0) ? shfl_up1(w1) : shfl_dn1(w0);
       const R mid = radd(w0, w1);
@@ -360,104 +394,154 @@ struct WavePipe {
       const R weB = (O == 0) ? mid : radd(w1, nb);
       R v0 = sor_update(radd(n0, s0), weA, u0, a.w);
       R v1 = sor_update(radd(n1, s1), weB, u1, a.w);
-      v0 = (rowok && upd[O]) ? v0 : u0;
-      v1 = (rowok && upd[O + 2]) ? v1 : u1;
-      if (CHECK && s >= S - 2) {
-        if (r >= R0 && r < R1 && rowok) {
-          if (own[O]) dmax = umax64(dmax, delta_bits(v0, u0));
-          if (own[O + 2]) dmax = umax64(dmax, delta_bits(v1, u1));
+      if (MASK) {
+        const bool rowok = (unsigned)(r - 1) < (unsigned)rows;
+        v0 = (rowok && upd[O]) ? v0 : u0;
+        v1 = (rowok && upd[O + 2]) ? v1 : u1;
+      }
+      if (CK != 0 && (CK == 2 || s >= S - 2)) {
+        if (r >= R0 && r < R1) {
+          const int slot = CK == 2 ? (s >> 1) : 0;
+          if (own[O]) dmax[slot] = umax64(dmax[slot], delta_bits(v0, u0));
+          if (own[O + 2]) dmax[slot] = umax64(dmax[slot], delta_bits(v1, u1));
         }
       }
       if (s < S - 1) {
-        C[s][0][0] = v0;
-        C[s][0][1] = v1;
-      } else {
-        // finished row r: this stage's colour at q = O, O+2, the other colour
-        // from stage S-2's row r (computed one step ago at q = 1-O, 3-O)
-        if (r >= R0 && r < R1 && rowok) {
-          R out[4];
-          out[O] = v0;
-          out[O + 2] = v1;
-          out[1 - O] = C[S - 2][1][0];
-          out[3 - O] = C[S - 2][1][1];
-          R* p = a.dst + (r - a.g0) * a.pitch + c0;
-          if (own_all) {
-            stg4(p, out);
-          } else {
+        C[s][PH][0] = v0;
+        C[s][PH][1] = v1;
+      } else if (r >= R0 && r < R1) {
+        // finished row r: this stage's colour at q = O, O+2; the other colour
+        // from stage S-2's row r (one step old, at q = 1-O, 3-O)
+        R out[4];
+        out[O] = v0;
+        out[O + 2] = v1;
+        out[1 - O] = C[S - 2][P1][0];
+        out[3 - O] = C[S - 2][P1][1];
+        R* p = a.dst + (long long)(r - a.g0) * a.pitch + c0;
+        if (own_all) {
+          stg4(p, out);
+        } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (own[q]) p[q] = out[q];
-          }
+          for (int q = 0; q < 4; ++q)
+            if (own[q]) p[q] = out[q];
         }
       }
     }
   }
+
+  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, int nsteps, long long c0) {
+#pragma unroll 1
+    for (int m = 0; m < nsteps; m += 6) {
+      step<0>(a, i_first + m, m, c0);
+      step<1>(a, i_first + m + 1, m + 1, c0);
+      step<2>(a, i_first + m + 2, m + 2, c0);
+      step<3>(a, i_first + m + 3, m + 3, c0);
+      step<4>(a, i_first + m + 4, m + 4, c0);
+      step<5>(a, i_first + m + 5, m + 5, c0);
+    }
+  }
 };
 
-template <typename R, int T, int NST, bool CHECK>
-__global__ void __launch_bounds__(kWaveWarps * 32) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
+// One warp = one (strip, band) tile; warps never synchronise with each other.
+template <typename R, int T, int NST, int CK, bool MASK>
+__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* wbase, int lane,
+                                          int sw, int R0, int R1, int i_first, int nsteps,
+                                          unsigned long long (&dm)[kMaxT]) {
+  WavePipe<R, T, NST, CK, MASK> P;
+#pragma unroll
+  for (int t = 0; t < P.NSLOT; ++t) P.dmax[t] = 0ull;
+  P.ring = reinterpret_cast<const R*>(wbase);
+  P.ring_s = smem_u32(wbase);
+  P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
+  P.lane = lane;
+  P.rows = (int)a.rows;
+  P.R0 = R0;
+  P.R1 = R1;
+  const long long c0 = (long long)sw + 4 * lane;
+  const int olo = max(sw + 2 * T, 1);
+  const int ohi = min(sw + kWaveCols - 2 * T, (int)a.cols + 1);
+  P.own_all = true;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = (int)c0 + q;
+    P.upd[q] = (c >= 1) && (c <= (int)a.cols);
+    P.own[q] = (c >= olo) && (c < ohi);
+    P.own_all = P.own_all && P.own[q];
+  }
+#pragma unroll
+  for (int s = 0; s < 2 * T - 1; ++s)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
+  P.pitch = a.pitch;
+  P.gsrc = a.src + (long long)(i_first - 1 - a.g0) * a.pitch + sw;
+  P.n_total = nsteps + 2;
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < NST; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < NST; ++k)
+      if (k < P.n_total) P.issue(k);
+  }
+  P.consume(0, P.F[0]);  // row i_first - 1
+  P.consume(1, P.F[1]);  // row i_first
+  P.run(a, i_first, nsteps, c0);
+#pragma unroll
+  for (int t = 0; t < P.NSLOT; ++t) dm[t] = P.dmax[t];
+}
+
+// Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines.
+__host__ __device__ constexpr int wave_min_blocks(int T) { return T <= 2 ? 4 : 3; }
+
+template <typename R, int T, int NST, int CK>
+__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
   extern __shared__ __align__(128) unsigned char wave_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWaveWarps + warp;
-  WavePipe<R, T, NST, CHECK> P;
-  P.dmax = 0ull;
+  unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
   if (gw < a.nstrips * a.nbands) {
-    unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
-    P.ring = reinterpret_cast<const R*>(wbase);
-    P.ring_s = smem_u32(wbase);
-    P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
-    P.lane = lane;
     const int strip = gw % a.nstrips;
     const int band = gw / a.nstrips;
-    const long long sw = a.s0 + (long long)strip * (kWaveCols - 4 * T);
-    const long long c0 = sw + 4 * lane;
-    const long long R0 = a.r_lo + (long long)band * a.band_h;
-    const long long R1 = min(R0 + a.band_h, a.r_hi);
-    const long long olo = max(sw + 2 * T, 1LL);
-    const long long ohi = min(sw + kWaveCols - 2 * T, a.cols + 1);
-    P.own_all = true;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const long long c = c0 + q;
-      P.upd[q] = (c >= 1) && (c <= a.cols);
-      P.own[q] = (c >= olo) && (c < ohi);
-      P.own_all = P.own_all && P.own[q];
-    }
-#pragma unroll
-    for (int s = 0; s < 2 * T - 1; ++s)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
-    // steps i = i_first .. (even start; stage 2T-1 reaches row R0 after 2T-1
-    // warm-up rows); step i consumes src row i+1.  Rows streamed: i_first-1 ..
-    const long long i_first = (R0 - (2 * T - 1)) & ~1LL;
-    const long long nsteps = ((R1 + 2 * T - 1 - i_first) + 1) & ~1LL;
-    P.pitch = a.pitch;
-    P.gsrc = a.src + (i_first - 1 - a.g0) * a.pitch + sw;
-    P.n_total = nsteps + 2;
-    if (lane == 0) {
-#pragma unroll 1
-      for (int k = 0; k < NST; ++k) mbar_init(P.bar_s + 8u * k, 1u);
-      mbar_fence_init();
-    }
-    __syncwarp();
-    if (lane == 0) {
-#pragma unroll 1
-      for (int k = 0; k < NST; ++k)
-        if (k < P.n_total) P.issue(k);
-    }
-    P.consume(0, P.F[1]);  // row i_first - 1
-    P.consume(1, P.F[2]);  // row i_first
-#pragma unroll 1
-    for (long long m = 0; m < nsteps; m += 2) {
-      P.template step<0>(a, i_first + m, m + 2, c0, R0, R1);
-      P.template step<1>(a, i_first + m + 1, m + 3, c0, R0, R1);
-    }
+    const int sw = a.s0 + strip * (kWaveCols - 4 * T);
+    const int R0 = (int)a.r_lo + band * (int)a.band_h;
+    const int R1 = min(R0 + (int)a.band_h, (int)a.r_hi);
+    // step m (front row i_first+m) feeds stage 2T-1 row i_first+m-2T+1;
+    // i_first even; nsteps a multiple of 6 (ring phase x parity)
+    const int i_first = (R0 - (2 * T - 1)) & ~1;
+    const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
+    const bool interior = (sw >= 1) && (sw + kWaveCols - 1 <= (int)a.cols) && (i_first - 1 >= 1) &&
+                          (i_first + nsteps <= (int)a.rows);
+    unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
+    if (interior)
+      wave_tile<R, T, NST, CK, false>(a, wbase, lane, sw, R0, R1, i_first, nsteps, dm);
+    else
+      wave_tile<R, T, NST, CK, true>(a, wbase, lane, sw, R0, R1, i_first, nsteps, dm);
   }
-  if (CHECK) {
-    const unsigned long long m = warp_max_u64(P.dmax);
-    if (lane == 0) contribute_and_maybe_finalize(ctl, m);
+  if (CK != 0) {
+    // warp max -> CTA max in shared memory -> one atomic per CTA and slot
+    constexpr int NS = CK == 2 ? T : 1;
+    __shared__ unsigned long long cta_max[kWaveWarps][NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const unsigned long long m = warp_max_u64(dm[t]);
+      if (lane == 0) cta_max[warp][t] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        unsigned long long m = 0ull;
+#pragma unroll
+        for (int w = 0; w < kWaveWarps; ++w) m = umax64(m, cta_max[w][t]);
+        contribute(ctl, t, m);
+      }
+      maybe_finalize(ctl);
+    }
   }
 }
 
