@@ -458,7 +458,7 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
 
 // ------------------------------------------------------------------ K3/K4
 template <typename R>
-constexpr int wave_nst() { return sizeof(R) == 8 ? 8 : 12; }
+constexpr int wave_nst() { return 12; }
 
 template <typename R, int T, int CK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {

@@ -299,11 +299,35 @@ __device__ __forceinline__ void lds4(const float* p, float (&x)[4]) {
   x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
 }
 
-// Shared memory of wave_kernel per warp: NST row slots of kWaveCols values,
-// then NST mbarriers.
+// Shared memory of wave_kernel per warp: 2 batches of 6 source rows (12 slots
+// of kWaveCols values; the 2 prologue rows borrow the last two slots of batch
+// 1 until they are read), then 3 mbarriers (one per batch, one for the
+// prologue).  NST is the number of row slots (12).
 template <typename R, int NST>
 __host__ __device__ constexpr int wave_smem_per_warp() {
-  return NST * kWaveCols * (int)sizeof(R) + NST * 8;
+  return (NST * kWaveCols * (int)sizeof(R) + 3 * 8 + 127) / 128 * 128;  // 128-B aligned bases
+}
+
+// Predicated stores (branch-free, so unrolled steps form one basic block).
+__device__ __forceinline__ void stg4_if(bool p, double* a, const double (&x)[4]) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f64 [%0], {%1,%2,%3,%4};\n}" ::"l"(a),
+               "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3]), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ void stg4_if(bool p, float* a, const float (&x)[4]) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f32 [%0], {%1,%2,%3,%4};\n}" ::"l"(a),
+               "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ void stg1_if(bool p, double* a, double x) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(a), "d"(x),
+               "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(a), "f"(x),
+               "r"((int)p)
+               : "memory");
 }
 
 // Register pipeline of one warp.
@@ -333,38 +357,39 @@ struct WavePipe {
   bool upd[4], own[4];
   bool own_all;
   int rows, R0, R1;
-  // ring
+  // ring: row n >= 2 in batch j = (n-2)/6, slot (j&1)*6 + (n-2)%6, barrier
+  // j&1 (phase (j>>1)&1); rows n = 0,1 (prologue) first use slots 10, 11
   const R* ring;
   uint32_t ring_s, bar_s;
   const R* gsrc;              // global address of (row i_first-1, column s_w)
   long long pitch;
-  int n_total;
+  int nbatch;
   int lane;
+  static constexpr uint32_t ROWB = kWaveCols * sizeof(R);
 
-  __device__ __forceinline__ void issue(int n) {  // lane 0: row i_first-1+n -> slot n % NST
-    const int slot = n % NST;
-    const uint32_t bar = bar_s + 8u * slot;
-    mbar_expect_tx(bar, kWaveCols * sizeof(R));
-    bulk_g2s(ring_s + slot * kWaveCols * sizeof(R), gsrc + (long long)n * pitch, kWaveCols * sizeof(R), bar);
+  // lane 0: rows k_lo..k_hi-1 of batch j (expect_tx covers the whole batch
+  // when k_lo == 0; a second call completes it)
+  __device__ __forceinline__ void issue_batch(int j, int k_lo = 0, int k_hi = 6) {
+    const uint32_t bar = bar_s + 8u * (j & 1);
+    if (k_lo == 0) mbar_expect_tx(bar, 6 * ROWB);
+#pragma unroll 1
+    for (int k = k_lo; k < k_hi; ++k)
+      bulk_g2s(ring_s + ((j & 1) * 6 + k) * ROWB, gsrc + (long long)(6 * j + 2 + k) * pitch, ROWB, bar);
   }
-  __device__ __forceinline__ void consume(int n, R (&x)[4]) {
-    const int slot = n % NST;
-    mbar_wait(bar_s + 8u * slot, (uint32_t)((n / NST) & 1));
-    lds4(ring + slot * kWaveCols + 4 * lane, x);
-    __syncwarp();
-    if (lane == 0 && n + NST < n_total) {
-      fence_proxy_async_smem();
-      issue(n + NST);
-    }
+  __device__ __forceinline__ void issue_prologue() {  // lane 0
+    const uint32_t bar = bar_s + 16u;
+    mbar_expect_tx(bar, 2 * ROWB);
+    bulk_g2s(ring_s + 10 * ROWB, gsrc, ROWB, bar);
+    bulk_g2s(ring_s + 11 * ROWB, gsrc + pitch, ROWB, bar);
   }
 
   template <int M6>
-  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, int m, long long c0) {
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, long long c0) {
     constexpr int O = M6 & 1;
     constexpr int PH = M6 % 3;          // slot of age 0 (this step)
     constexpr int P1 = (PH + 2) % 3;    // age 1
     constexpr int P2 = (PH + 1) % 3;    // age 2
-    consume(m + 2, F[P1]);              // source row i+1 (slot (m+2)%3)
+    lds4(rowp + M6 * kWaveCols, F[P1]); // source row i+1 (ring slot (m+2)%3)
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int r = i - s;
@@ -400,44 +425,51 @@ struct WavePipe {
         v1 = (rowok && upd[O + 2]) ? v1 : u1;
       }
       if (CK != 0 && (CK == 2 || s >= S - 2)) {
-        if (r >= R0 && r < R1) {
-          const int slot = CK == 2 ? (s >> 1) : 0;
-          if (own[O]) dmax[slot] = umax64(dmax[slot], delta_bits(v0, u0));
-          if (own[O + 2]) dmax[slot] = umax64(dmax[slot], delta_bits(v1, u1));
-        }
+        const bool inb = (r >= R0) & (r < R1);
+        const int slot = CK == 2 ? (s >> 1) : 0;
+        const unsigned long long d0 = delta_bits(v0, u0), d1 = delta_bits(v1, u1);
+        dmax[slot] = umax64(dmax[slot], (inb && own[O]) ? d0 : 0ull);
+        dmax[slot] = umax64(dmax[slot], (inb && own[O + 2]) ? d1 : 0ull);
       }
       if (s < S - 1) {
         C[s][PH][0] = v0;
         C[s][PH][1] = v1;
-      } else if (r >= R0 && r < R1) {
+      } else {
         // finished row r: this stage's colour at q = O, O+2; the other colour
         // from stage S-2's row r (one step old, at q = 1-O, 3-O)
+        const bool inb = (r >= R0) & (r < R1);
         R out[4];
         out[O] = v0;
         out[O + 2] = v1;
         out[1 - O] = C[S - 2][P1][0];
         out[3 - O] = C[S - 2][P1][1];
         R* p = a.dst + (long long)(r - a.g0) * a.pitch + c0;
-        if (own_all) {
-          stg4(p, out);
-        } else {
+        stg4_if(inb && own_all, p, out);
+        if (!own_all) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (own[q]) p[q] = out[q];
+          for (int q = 0; q < 4; ++q) stg1_if(inb && own[q], p + q, out[q]);
         }
       }
     }
   }
 
-  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, int nsteps, long long c0) {
+  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, long long c0) {
 #pragma unroll 1
-    for (int m = 0; m < nsteps; m += 6) {
-      step<0>(a, i_first + m, m, c0);
-      step<1>(a, i_first + m + 1, m + 1, c0);
-      step<2>(a, i_first + m + 2, m + 2, c0);
-      step<3>(a, i_first + m + 3, m + 3, c0);
-      step<4>(a, i_first + m + 4, m + 4, c0);
-      step<5>(a, i_first + m + 5, m + 5, c0);
+    for (int j = 0; j < nbatch; ++j) {
+      const int m = 6 * j;
+      mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
+      const R* rowp = ring + (j & 1) * 6 * kWaveCols + 4 * lane;
+      step<0>(a, i_first + m, rowp, c0);
+      step<1>(a, i_first + m + 1, rowp, c0);
+      step<2>(a, i_first + m + 2, rowp, c0);
+      step<3>(a, i_first + m + 3, rowp, c0);
+      step<4>(a, i_first + m + 4, rowp, c0);
+      step<5>(a, i_first + m + 5, rowp, c0);
+      __syncwarp();
+      if (lane == 0 && j + 2 < nbatch) {
+        fence_proxy_async_smem();  // our generic reads of the slots precede the async refill
+        issue_batch(j + 2);
+      }
     }
   }
 };
@@ -453,6 +485,7 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
   P.ring = reinterpret_cast<const R*>(wbase);
   P.ring_s = smem_u32(wbase);
   P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
+  static_assert(NST == 12, "ring layout: 2 batches of 6 rows");
   P.lane = lane;
   P.rows = (int)a.rows;
   P.R0 = R0;
@@ -474,21 +507,27 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
     for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
   P.pitch = a.pitch;
   P.gsrc = a.src + (long long)(i_first - 1 - a.g0) * a.pitch + sw;
-  P.n_total = nsteps + 2;
+  P.nbatch = nsteps / 6;
   if (lane == 0) {
-#pragma unroll 1
-    for (int k = 0; k < NST; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mbar_init(P.bar_s + 8u * k, 1u);
     mbar_fence_init();
   }
   __syncwarp();
   if (lane == 0) {
-#pragma unroll 1
-    for (int k = 0; k < NST; ++k)
-      if (k < P.n_total) P.issue(k);
+    P.issue_prologue();
+    P.issue_batch(0);
+    if (P.nbatch > 1) P.issue_batch(1, 0, 4);
   }
-  P.consume(0, P.F[0]);  // row i_first - 1
-  P.consume(1, P.F[1]);  // row i_first
-  P.run(a, i_first, nsteps, c0);
+  mbar_wait(P.bar_s + 16u, 0u);
+  lds4(P.ring + 10 * kWaveCols + 4 * lane, P.F[0]);  // row i_first - 1
+  lds4(P.ring + 11 * kWaveCols + 4 * lane, P.F[1]);  // row i_first
+  __syncwarp();
+  if (lane == 0 && P.nbatch > 1) {
+    fence_proxy_async_smem();
+    P.issue_batch(1, 4, 6);
+  }
+  P.run(a, i_first, c0);
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) dm[t] = P.dmax[t];
 }
