@@ -534,6 +534,7 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
 
 template <typename R, int CK>
 int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool fused_fin) {
+  if (CK == 3 && T == 1) return launch_wave_T<R, 1, 2>(g, s, w, ctl, fused_fin);  // unused combination
   switch (T) {
     case 1: return launch_wave_T<R, 1, CK>(g, s, w, ctl, fused_fin);
     case 2: return launch_wave_T<R, 2, CK>(g, s, w, ctl, fused_fin);
@@ -550,7 +551,9 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   const bool fused_fin = single_part(g) && ctl.ck != 0;
   if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
   for (auto& s : g->slabs) {
-    if (ctl.ck == 2)
+    if (ctl.ck == 3)
+      TRY((launch_wave<R, 3>(g, s, T, w, ctl, fused_fin)));
+    else if (ctl.ck == 2)
       TRY((launch_wave<R, 2>(g, s, T, w, ctl, fused_fin)));
     else if (ctl.ck == 1)
       TRY((launch_wave<R, 1>(g, s, T, w, ctl, fused_fin)));
@@ -648,7 +651,7 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
       IterCtl c = base;
       c.k_last = k + t - 1;
       c.T = t;
-      c.ck = every ? 2 : (c.k_last == next_check ? 1 : 0);
+      c.ck = every ? 3 : (c.k_last == next_check ? 1 : 0);
       TRY(wave_pass<R>(g, w, c));
       if (c.ck) g->st.checks += every ? t : 1;
       k += t;
@@ -681,17 +684,60 @@ int iterate_impl(sor_grid* g, double omega, int64_t iters, double* last) {
   return SOR_OK;
 }
 
+int read_state(sor_grid* g, DevState* out) {
+  CU(cudaMemcpyAsync(&g->hstate[0], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  *out = g->hstate[0];
+  return SOR_OK;
+}
+
+// The pass of this solve segment that contains iteration k: (k_end, cur after, depth).
+bool find_pass(const sor_grid* g, int64_t k, int64_t* k_end, int* cur_after, int* tp) {
+  for (const auto& pe : g->pass_ends) {
+    if (k <= pe.first && k > pe.first - pe.second.second) {
+      *k_end = pe.first;
+      *cur_after = pe.second.first;
+      *tp = pe.second.second;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Re-run the first `depth` iterations of the pass that ended at k_end from its
+// source plane (untouched: later passes of the segment exited early), with
+// the exact max-change of its last iteration (ck=1) or of every iteration
+// (ck=2, solve semantics).  Leaves g->cur on the plane holding the result.
+template <typename R>
+int rerun_pass(sor_grid* g, R w, const IterCtl& base, int64_t k_end, int cur_after, int tp, int depth,
+               int ck, DevState* out) {
+  CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
+  g->cur = cur_after ^ 1;
+  IterCtl c = base;
+  c.k_last = k_end - tp + depth;
+  c.T = depth;
+  c.ck = ck;
+  c.solve = ck == 2 ? 1 : 0;
+  TRY(wave_pass<R>(g, w, c));
+  return read_state(g, out);
+}
+
 template <typename R>
 int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, int64_t* iters_out,
                double* max_out) {
   TRY(begin_call(g));
   const R w = (R)omega;
   DevState hs{};
+  bool converged = false;
+  int64_t done = maxit;
+  double maxc = 0.0;
   if (g->kernel == SOR_KERNEL_SMALL) {
     TRY(k5_run<R>(g, w, 1, maxit, tol, K, 0));
     TRY(end_call(g, &hs));
-    g->st.half_sweeps = 2 * hs.iters_done;
     g->st.checks = hs.checks;
+    converged = hs.converged != 0;
+    done = converged ? hs.conv_iter : maxit;
+    maxc = hs.max_change;
   } else {
     IterCtl base{};
     base.st = g->dstate;
@@ -699,68 +745,97 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     base.K = K;
     base.tol = tol;
     base.solve = 1;
-    const int cur0 = g->cur;
+    {
+      uint64_t tb;
+      memcpy(&tb, &tol, 8);
+      base.tol_hi = (unsigned)(tb >> 32);
+    }
+    const bool fast = g->kernel != SOR_KERNEL_NATURAL && K == 1 && depth_of(g) > 1;  // ck=3 passes
     // batches of whole check blocks (and whole passes); poll one batch behind
     const int64_t unit = std::max<int64_t>(K, depth_of(g));
     const int64_t blk = std::max<int64_t>(unit, (int64_t)((64 + unit - 1) / unit) * unit);
     int64_t k = 1;
-    int b = 0;
-    while (k <= maxit) {
-      const int64_t k_to = std::min(maxit, k + blk - 1);
-      TRY(enqueue_range<R>(g, w, k, k_to, base, false));
-      CU(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
-                         g->stream));
-      CU(cudaEventRecord(g->poll_ev[b & 1], g->stream));
-      k = k_to + 1;
-      if (b >= 1) {
-        CU(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
-        if (g->hstate[(b - 1) & 1].stop) break;
+    int64_t checks = 0;
+    while (true) {
+      // one segment: iterations k..maxit until the device stops the loop
+      CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
+      g->pass_ends.clear();
+      int b = 0;
+      for (int64_t kk = k; kk <= maxit;) {
+        const int64_t k_to = std::min(maxit, kk + blk - 1);
+        TRY(enqueue_range<R>(g, w, kk, k_to, base, false));
+        CU(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                           g->stream));
+        CU(cudaEventRecord(g->poll_ev[b & 1], g->stream));
+        kk = k_to + 1;
+        if (b >= 1) {
+          CU(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
+          if (g->hstate[(b - 1) & 1].stop) break;
+        }
+        ++b;
       }
-      ++b;
-    }
-    TRY(end_call(g, &hs));
-    const int64_t done = hs.converged ? hs.conv_iter : maxit;
-    // Which plane holds X_done.  Early-exited launches wrote nothing, but the
-    // host flipped cur for every pass it enqueued.  If the converging
-    // iteration sits inside a T-deep pass (ck = 2), X_done never reached HBM:
-    // re-run the first conv_t+1 iterations of that pass from its source
-    // plane, which no later (early-exited) pass has overwritten.
-    if (g->kernel != SOR_KERNEL_NATURAL) {
-      int c = cur0;
-      for (size_t q = 0; q < g->pass_ends.size(); ++q) {
-        const auto& pe = g->pass_ends[q];
-        const int64_t k_end = pe.first;
-        const int tp = pe.second.second;
-        if (done <= k_end && done > k_end - tp) {
-          c = pe.second.first;
-          if (done != k_end) {
-            g->cur = c ^ 1;  // the pass's source plane
-            IterCtl r{};
-            r.st = nullptr;
-            r.k_last = done;
-            r.T = (int)(done - (k_end - tp));
-            r.ck = 0;
-            r.solve = 0;
-            const auto saved = g->pass_ends;
-            const auto saved_st = g->st;
-            TRY(wave_pass<R>(g, w, r));
-            g->pass_ends = saved;
-            g->st = saved_st;
-            g->st.kernel_launches += (int64_t)g->slabs.size();
-            CU(cudaStreamSynchronize(g->stream));
-            c = g->cur;
-          }
+      TRY(read_state(g, &hs));
+      checks += hs.checks;
+      if (g->kernel == SOR_KERNEL_NATURAL) {  // in place, exact checks: nothing to redo
+        converged = hs.converged != 0;
+        done = converged ? hs.conv_iter : maxit;
+        maxc = hs.max_change;
+        break;
+      }
+      int64_t k_end = 0;
+      int cur_after = g->cur, tp = 1;
+      if (hs.ambiguous) {
+        // high words tied with tol's: decide this pass exactly
+        if (!find_pass(g, hs.amb_iter, &k_end, &cur_after, &tp))
+          return set_error(g, SOR_E_STATE, "internal: pass of iteration %lld not found", (long long)hs.amb_iter);
+        checks -= (hs.amb_iter - (k_end - tp + 1)) + 1;  // the exact pass re-counts them
+        DevState ex{};
+        TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, tp, 2, &ex));
+        if (ex.converged) {
+          checks += ex.checks;
+          converged = true;
+          done = ex.conv_iter;
+          const int depth = (int)(done - (k_end - tp));
+          DevState fin{};
+          TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, depth, 1, &fin));
+          maxc = fin.max_change;
           break;
         }
+        checks += ex.checks;
+        maxc = ex.max_change;
+        k = k_end + 1;  // g->cur now holds X_{k_end}
+        if (k > maxit) {
+          done = maxit;
+          break;
+        }
+        continue;
       }
-      g->cur = c;
+      if (hs.converged) {
+        converged = true;
+        done = hs.conv_iter;
+      } else {
+        done = maxit;
+      }
+      if (!find_pass(g, done, &k_end, &cur_after, &tp))
+        return set_error(g, SOR_E_STATE, "internal: pass of iteration %lld not found", (long long)done);
+      if (fast) {
+        // X_done and its exact max-change: re-run the pass up to `done`
+        DevState fin{};
+        TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, (int)(done - (k_end - tp)), 1, &fin));
+        maxc = fin.max_change;
+      } else {
+        g->cur = cur_after;  // passes end on checked iterations
+        maxc = hs.max_change;
+      }
+      break;
     }
-    g->st.half_sweeps = 2 * done;
-    hs.iters_done = done;
+    TRY(end_call(g, &hs));
+    g->st.checks = checks;
   }
-  if (iters_out) *iters_out = hs.converged ? hs.conv_iter : maxit;
-  if (max_out) *max_out = hs.max_change;
-  return hs.converged ? SOR_OK : SOR_NOT_CONVERGED;
+  g->st.half_sweeps = 2 * done;
+  if (iters_out) *iters_out = converged ? done : maxit;
+  if (max_out) *max_out = maxc;
+  return converged ? SOR_OK : SOR_NOT_CONVERGED;
 }
 
 int validate_omega(double omega) {

@@ -48,6 +48,8 @@ struct DevState {
   int stop;                    // solve: converged or maxit reached -> later launches exit
   int converged;
   int conv_t;                  // index within its pass of the converging iteration
+  int ambiguous;               // ck=3: a hi-word max tied with tol's; host resolves exactly
+  long long amb_iter;
   long long iters_done;        // iterations finished in this call
   long long conv_iter;
   long long checks;
@@ -62,7 +64,10 @@ struct IterCtl {
   long long K;          // check_every (solve)
   double tol;
   int T;                // iterations in this pass
-  int ck;               // 0: no max-change; 1: of iteration k_last; 2: of every iteration
+  int ck;               // 0: no max-change; 1: exact, of iteration k_last; 2: exact, of every
+                        // iteration; 3: high 32 bits only, of every iteration (stop decision
+                        // exact unless the high words tie with tol's -> ambiguous)
+  unsigned int tol_hi;  // high 32 bits of tol (ck=3)
   int solve;            // apply the stop test / early exit
   int finalize;         // this launch's last part runs the stop test
   unsigned int nparts;  // number of ticket takers (warps or CTAs) in this launch
@@ -93,6 +98,11 @@ __device__ __forceinline__ unsigned long long delta_bits(double un, double u) {
 __device__ __forceinline__ unsigned long long delta_bits(float un, float u) {
   return (unsigned long long)__double_as_longlong((double)fabsf(rsub(un, u)));
 }
+__device__ __forceinline__ int hi_bits(double x) { return __double2hiint(x); }
+__device__ __forceinline__ int hi_bits(float x) { return __double2hiint((double)x); }
+__device__ __forceinline__ unsigned int max3u(unsigned int a, unsigned int b, unsigned int c) {
+  return max(a, max(b, c));
+}
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
   return a > b ? a : b;
 }
@@ -113,9 +123,32 @@ __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) 
   st->ticket = 0u;
   for (int t = 0; t < ctl.T; ++t) {
     const long long k = k0 + t;
-    const int slot = ctl.ck == 2 ? t : 0;
-    const bool checked = ctl.ck == 2 ? (!ctl.solve || k % ctl.K == 0) : (t == ctl.T - 1);
+    const bool every = ctl.ck >= 2;
+    const int slot = every ? t : 0;
+    const bool checked = every ? (!ctl.solve || k % ctl.K == 0) : (t == ctl.T - 1);
     if (!checked) continue;
+    if (ctl.ck == 3) {
+      // non-negative doubles order like their bit patterns: a smaller high
+      // word decides '<', a larger one '>='; equal high words are ambiguous
+      const unsigned int h = (unsigned int)(st->maxbits[slot][0] >> 32);
+      st->checks += 1;
+      st->iters_done = k;
+      st->max_change = __longlong_as_double((long long)((unsigned long long)h << 32));
+      if (h < ctl.tol_hi) {
+        st->converged = 1;
+        st->conv_iter = k;
+        st->conv_t = t;
+        st->stop = 1;
+        break;
+      }
+      if (h == ctl.tol_hi) {
+        st->ambiguous = 1;
+        st->amb_iter = k;
+        st->stop = 1;
+        break;
+      }
+      continue;
+    }
     const double m = __longlong_as_double((long long)st->maxbits[slot][0]);
     st->checks += 1;
     st->max_change = m;
@@ -342,7 +375,8 @@ __device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
 // no value is ever moved.  Source rows arrive through an NST-deep shared
 // ring filled by TMA bulk copies issued NST rows ahead.
 //
-// CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each.
+// CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each,
+// 3 = high 32 bits of |delta| of each (VIMNMX3, ~1.5 ALU ops per cell).
 // MASK: false for warps whose rows and columns are all interior cells (no
 // Dirichlet/padding cell to keep fixed).  Ownership (which computed cells
 // are valid and written: the strip minus its 2T ghost columns on each side,
@@ -350,10 +384,11 @@ __device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
 template <typename R, int T, int NST, int CK, bool MASK>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
-  static constexpr int NSLOT = CK == 2 ? T : 1;
+  static constexpr int NSLOT = CK >= 2 ? T : 1;
   R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3
   R C[S - 1][3][2];           // stage outputs, slot = step % 3
-  unsigned long long dmax[NSLOT];
+  unsigned long long dmax[NSLOT];   // CK 1, 2: ordered bits; CK 3: high word in the low half
+  unsigned int ownA, ownB;         // CK 3: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
   bool upd[4], own[4];
   bool own_all;
   int rows, R0, R1;
@@ -424,7 +459,14 @@ struct WavePipe {
         v0 = (rowok && upd[O]) ? v0 : u0;
         v1 = (rowok && upd[O + 2]) ? v1 : u1;
       }
-      if (CK != 0 && (CK == 2 || s >= S - 2)) {
+      if (CK == 3) {
+        const bool inb = (r >= R0) & (r < R1);
+        const unsigned int mA = inb ? ownA : 0u, mB = inb ? ownB : 0u;
+        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & mA;
+        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & mB;
+        const int slot = s >> 1;
+        dmax[slot] = max3u((unsigned int)dmax[slot], hA, hB);
+      } else if (CK != 0 && (CK == 2 || s >= S - 2)) {
         const bool inb = (r >= R0) & (r < R1);
         const int slot = CK == 2 ? (s >> 1) : 0;
         const unsigned long long d0 = delta_bits(v0, u0), d1 = delta_bits(v1, u1);
@@ -501,6 +543,17 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
     P.own[q] = (c >= olo) && (c < ohi);
     P.own_all = P.own_all && P.own[q];
   }
+  // CK 3 excludes only the strip's ghost columns (invalid values); ring and
+  // padding cells are never updated, so their |delta| is 0 anyway.  Cell A is
+  // q = O in {0,1}, cell B is q = O+2 in {2,3}; the ghost bands are 2T wide
+  // and start at multiples of 4, so they cover whole pairs and A/B validity
+  // does not depend on O.
+  {
+    const int g_lo = sw + 2 * T, g_hi = sw + kWaveCols - 2 * T;
+    const int cA = (int)c0, cB = (int)c0 + 2;
+    P.ownA = (cA >= g_lo && cA + 1 < g_hi) ? 0x7fffffffu : 0u;
+    P.ownB = (cB >= g_lo && cB + 1 < g_hi) ? 0x7fffffffu : 0u;
+  }
 #pragma unroll
   for (int s = 0; s < 2 * T - 1; ++s)
 #pragma unroll
@@ -563,11 +616,13 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kern
   }
   if (CK != 0) {
     // warp max -> CTA max in shared memory -> one atomic per CTA and slot
-    constexpr int NS = CK == 2 ? T : 1;
+    constexpr int NS = CK >= 2 ? T : 1;
     __shared__ unsigned long long cta_max[kWaveWarps][NS];
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      const unsigned long long m = warp_max_u64(dm[t]);
+      const unsigned long long m =
+          CK == 3 ? ((unsigned long long)__reduce_max_sync(0xffffffffu, (unsigned int)dm[t]) << 32)
+                  : warp_max_u64(dm[t]);
       if (lane == 0) cta_max[warp][t] = m;
     }
     __syncthreads();

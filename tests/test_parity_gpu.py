@@ -211,3 +211,26 @@ def test_zero_iterations_and_stats(gpu):
         assert st["half_sweeps"] == 20 and st["hbm_passes"] == 3   # 2 + 4 + 4
         assert st["kernel_launches"] == 3
         assert g.elapsed_ms > 0
+
+
+@pytest.mark.parametrize("T", [2, 3, 4])
+@pytest.mark.parametrize("nudge", ["converge_here", "tie_continue"])
+def test_solve_high_word_tie_resolved_exactly(gpu, orc, T, nudge):
+    """ck=3 passes decide '<' on the high 32 bits; a tie must be resolved exactly."""
+    init = SI.random_edges(60, 75, seed=21)
+    probe = init.copy()
+    hist = [orc.iterate(probe, 1.9, 1, measure_last=True).max_change for _ in range(60)]
+    k = 41                                     # an iteration inside a pass
+    m = hist[k - 1]
+    assert min(hist[:k - 1]) > m               # no earlier iteration is below m
+    tol = float(np.nextafter(m, np.inf)) if nudge == "converge_here" else m
+    ref = init.copy()
+    rr = orc.solve(ref, 1.9, tol, 500, 1)
+    if nudge == "converge_here":
+        assert rr.converged and rr.iters == k
+    with gpu.Grid.create(init) as g:
+        g.set_kernel("temporal", T)
+        r = g.solve(1.9, tol, 500, 1)
+        out = g.download()
+    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
+    assert np.array_equal(out, ref)
