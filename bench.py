@@ -48,6 +48,11 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def g_nsm():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -169,7 +174,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--kernel", default="temporal")
-    ap.add_argument("--T", type=int, default=4)
+    ap.add_argument("--T", type=int, default=3)
     ap.add_argument("--no-solve", action="store_true", help="fixed iterations only")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-iters", type=int, default=32)
@@ -214,16 +219,21 @@ def main():
         st = g.stats
         n_iter = iters_fixed
         n_launch = st["kernel_launches"]
-        solve_iters = 0
+        solve_iters, t_sv, sv_launch, sv_passes = 0, 0.0, 0, 0
         if do_solve:
             r = g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every)
             solve_iters = r.iters
             n_iter += r.iters
-            n_launch += g.stats["kernel_launches"]
+            t_sv = g.elapsed_ms
+            s2 = g.stats
+            sv_launch = s2["kernel_launches"]
+            sv_passes = s2["hbm_passes"]
+            n_launch += sv_launch
         if record is not None:
             record.append({"iters": n_iter, "solve_iters": solve_iters, "t_iterate_ms": t_it,
                            "iterate_launches": st["kernel_launches"], "launches": n_launch,
-                           "hbm_passes": st["hbm_passes"]})
+                           "hbm_passes": st["hbm_passes"], "t_solve_ms": t_sv, "solve_launches": sv_launch,
+                           "solve_passes": sv_passes})
 
     def barrier():
         if world > 1:
@@ -254,21 +264,38 @@ def main():
     updates = cfg.rows * cfg.cols * iters_total
     value = updates / (ms_total * 1e-3) / 1e9
 
-    # dominant kernel roofline: the fixed-iteration phase launches only the
-    # wave kernel (one launch per HBM pass of T iterations)
+    # dominant kernel roofline.  Both phases launch one wave_kernel per HBM pass
+    # (the stop test is fused into it); the solve phase (per-iteration
+    # max-change, ck=3) takes most of the step when present.
     pk, pk_kind = peaks()
     esz = 8 if cfg.dtype == "f64" else 4
-    t_launch_ms = sum(r["t_iterate_ms"] for r in recs) / sum(r["iterate_launches"] for r in recs)
+    T_eff = args.T if args.kernel == "temporal" else 1
+    t_it_total = sum(r["t_iterate_ms"] for r in recs)
+    t_sv_total = sum(r["t_solve_ms"] for r in recs)
+    solve_dominant = t_sv_total > t_it_total
+    if solve_dominant:
+        t_launch_ms = t_sv_total / sum(r["solve_launches"] for r in recs)
+        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck={3 if T_eff > 1 else 1}> (solve phase)"
+    else:
+        t_launch_ms = t_it_total / sum(r["iterate_launches"] for r in recs)
+        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck=0> (fixed-iteration phase)"
     rows_local = g.stats["row_hi"] - g.stats["row_lo"]
     bytes_per_launch = 2 * esz * rows_local * cfg.cols          # read X_{k0} + write X_{k0+T}, once each
     achieved = bytes_per_launch / (t_launch_ms * 1e-3) / 1e9
-    it_glups = cfg.rows * cfg.cols * iters_fixed * len(recs) / (sum(r["t_iterate_ms"] for r in recs) * 1e-3) / 1e9
+    it_glups = cfg.rows * cfg.cols * iters_fixed * len(recs) / (t_it_total * 1e-3) / 1e9
+    sv_glups = (cfg.rows * cfg.cols * sum(r["solve_iters"] for r in recs) / (t_sv_total * 1e-3) / 1e9
+                if t_sv_total > 0 else None)
+    # FP64 pipe roofline of the same launch: 7 flops per update (+1 for |delta|
+    # when measured), peak = 148 SMs x 64 FP64 lanes x max SM clock
+    flops_per_update = 7 + (1 if solve_dominant else 0)
+    alu_peak = g_nsm() * 64 * 1.965e9 / 1e12
+    alu_achieved = flops_per_update * rows_local * cfg.cols * T_eff / (t_launch_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f)
-        key = f"{cfg.name}:{cfg.dtype}:{args.kernel}:{args.T}"
+        key = f"{cfg.name}:{kname}"
         if key in tr:
             traffic = tr[key]["dram_bytes_per_launch"]
 
@@ -288,12 +315,16 @@ def main():
             "parallelism": f"row-slab x{world}" if world > 1 else "single GPU",
         },
         "fixed_phase_glups": it_glups,
+        "solve_phase_glups": sv_glups,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                     "kernel": f"wave_kernel<{cfg.dtype},T={args.T if args.kernel == 'temporal' else 1}>",
+                     "kernel": kname,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": t_launch_ms, "peak_kind": pk_kind,
-                     "effective_frac_16B_per_update": it_glups * 2 * esz / pk["hbm_gbs"]},
+                     "effective_frac_16B_per_update": (value * 2 * esz) / pk["hbm_gbs"],
+                     "fp64_pipe": {"achieved_tflops": alu_achieved, "peak_tflops": alu_peak,
+                                   "frac": alu_achieved / alu_peak,
+                                   "note": "no FMA: each op is one FP64 instruction; peak = SMs x 64 x 1.965 GHz"}},
         "gpu_launches": sum(r["launches"] for r in recs),
         "clocks": ck,
     }
