@@ -1,0 +1,133 @@
+"""BASELINE.json configurations at FULL size through the C ABI vs the oracle (`-m gpu`).
+
+C1-C3 are compared element by element over the whole grid (the threaded
+oracle is bitwise the serial one, pin P14).  C4 and C5 are too large for the
+oracle to redo whole, so they are compared on sampled patches the oracle can
+compute exactly: after k iterations a cell depends only on cells within 2k
+rows/columns (one row or column per half-sweep), so a patch of the initial
+grid whose outer rows/columns act as a fixed ring reproduces the exact
+iterate at every cell farther than 2k from the patch's artificial edges.
+Patches sit at the four corners and the four edge midpoints (where the
+boundary data lives); the centre, more than 2k from every edge of the
+zero-initialised interior, must be exactly 0.  Launch configuration: the
+kernel bench.py times (temporal T=3) and K3.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import sor_inputs as SI
+
+pytestmark = pytest.mark.gpu
+THREADS = len(os.sched_getaffinity(0))
+
+
+@pytest.fixture(scope="module")
+def gpu(sor):
+    import torch
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    return sor
+
+
+def test_c1_full(gpu, orc):
+    cfg = SI.config("C1")
+    ref = cfg.init()
+    rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, 1)
+    assert rr.converged and rr.iters == 1785          # SURVEY P11 (derived), oracle authoritative
+    for kernel, T in (("small", 1), ("temporal", 3)):
+        with gpu.Grid.create(cfg.init()) as g:
+            g.set_kernel(kernel, T)
+            r = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1)
+            out = g.download()
+        assert (r.converged, r.iters, r.max_change) == (True, rr.iters, rr.max_change)
+        assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("kernel,T", [("temporal", 3), ("fused", 1)])
+def test_c2_full(gpu, orc, kernel, T):
+    cfg = SI.config("C2")
+    ref = cfg.init()
+    rep = orc.iterate(ref, cfg.omega, cfg.iters, measure_last=True, threads=THREADS)
+    with gpu.Grid.create(cfg.init()) as g:
+        g.set_kernel(kernel, T)
+        d = g.iterate(cfg.omega, cfg.iters, want_delta=True)
+        out = g.download()
+    assert np.array_equal(out, ref)
+    assert d == rep.max_change
+
+
+def test_c3_full_iterate_then_solve(gpu, orc):
+    """BJ configs[2] exactly as bench.py runs it: iterate(1000) then solve(1e-8, K=1)."""
+    cfg = SI.config("C3")
+    ref = cfg.init()
+    rep = orc.iterate(ref, cfg.omega, cfg.iters, measure_last=True, threads=THREADS)
+    with gpu.Grid.create(cfg.init()) as g:
+        g.set_kernel("temporal", 3)
+        d = g.iterate(cfg.omega, cfg.iters, want_delta=True)
+        mid = g.download()
+        assert np.array_equal(mid, ref) and d == rep.max_change
+        rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, 1, threads=THREADS)
+        r = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1)
+        out = g.download()
+    assert rr.converged and rr.iters == 12480          # SURVEY P11 / reading R21
+    assert (r.converged, r.iters, r.max_change) == (True, rr.iters, rr.max_change)
+    assert np.array_equal(out, ref)
+
+
+def _patch_oracle(orc, init, dtype, omega, iters, r0, r1, c0, c1):
+    """Exact iterate on [r0+m, r1-m) x [c0+m, c1-m) (m = margin where fake)."""
+    assert c0 % 2 == 0 and r0 % 2 == 0                 # keep the colour of (i, j): parity of i+j
+    p = orc.to_storage(init[r0:r1, c0:c1], dtype)
+    orc.iterate(p, omega, iters, threads=THREADS)      # threaded == serial bitwise (P14)
+    return p.astype(np.float64)
+
+
+def _check_patches(gpu, orc, cfg, g, dtype, P):
+    rows, cols, k = cfg.rows, cfg.cols, cfg.iters
+    m = 2 * k + 2                                      # dependency cone + safety
+    init = cfg.init()
+    R, C = rows + 2, cols + 2
+    assert P % 2 == 0 and R % 2 == 0 and C % 2 == 0
+    spans_r = [(0, P), (R - P, R), ((R // 2 - P // 2) & ~1, ((R // 2 - P // 2) & ~1) + P)]
+    spans_c = [(0, P), (C - P, C), ((C // 2 - P // 2) & ~1, ((C // 2 - P // 2) & ~1) + P)]
+    checked = 0
+    for (r0, r1) in spans_r:
+        for (c0, c1) in spans_c:
+            if (r0, c0) == (spans_r[2][0], spans_c[2][0]):
+                continue                               # the centre: checked separately
+            exact = _patch_oracle(orc, init, dtype, cfg.omega, k, r0, r1, c0, c1)
+            got = g.download_rows(r0, r1)[:, c0:c1]
+            # valid region: away from artificial patch edges (real ring edges are exact)
+            a = 0 if r0 == 0 else m
+            b = (r1 - r0) if r1 == R else (r1 - r0) - m
+            lft = 0 if c0 == 0 else m
+            rgt = (c1 - c0) if c1 == C else (c1 - c0) - m
+            assert b > a and rgt > lft
+            assert np.array_equal(got[a:b, lft:rgt], exact[a:b, lft:rgt]), (r0, c0)
+            checked += (b - a) * (rgt - lft)
+    # centre: more than 2k from every ring cell -> still exactly the initial 0
+    cr = R // 2
+    mid = g.download_rows(cr - 4, cr + 4)
+    assert not mid[:, m:C - m].any()
+    return checked
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_c4_full_sampled(gpu, orc, dtype):
+    cfg = SI.config("C4", dtype=dtype)
+    with gpu.Grid.create(cfg.init(), dtype=dtype) as g:
+        g.set_kernel("temporal", 3)
+        g.iterate(cfg.omega, cfg.iters)
+        n = _check_patches(gpu, orc, cfg, g, dtype, P=2 * (2 * cfg.iters + 2) + 256)
+    assert n > 4 * 256 * 256
+
+
+def test_c5_full_sampled(gpu, orc):
+    cfg = SI.config("C5")
+    with gpu.Grid.create(cfg.init()) as g:
+        g.set_kernel("temporal", 3)
+        g.iterate(cfg.omega, cfg.iters)
+        n = _check_patches(gpu, orc, cfg, g, "f64", P=2 * (2 * cfg.iters + 2) + 512)
+    assert n > 4 * 512 * 512
