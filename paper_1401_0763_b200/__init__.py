@@ -59,7 +59,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = LIB
+    path = os.environ.get("SOR_LIBRARY", LIB)   # development: alternative builds of libsor
     if not os.path.exists(path):
         if not build_if_missing:
             raise FileNotFoundError(f"{path} not built; run __graft_entry__.build()")

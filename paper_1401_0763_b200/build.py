@@ -42,19 +42,19 @@ def sources() -> list[str]:
                   + [os.path.join(INCLUDE, "sor.h")])
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
-    stale = not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(s) for s in sources())
+def build_lib(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    stale = not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(s) for s in sources())
     if not (force or stale):
-        return LIB
+        return out
     nc = nccl_dir()
-    cmd = [NVCC, *NVCC_FLAGS, "-I" + INCLUDE, "-I" + os.path.join(nc, "include"),
-           os.path.join(CSRC, "sor_api.cu"), "-o", LIB + ".tmp",
+    cmd = [NVCC, *NVCC_FLAGS, *("-D" + d for d in defines), "-I" + INCLUDE, "-I" + os.path.join(nc, "include"),
+           os.path.join(CSRC, "sor_api.cu"), "-o", out + ".tmp",
            "-L" + os.path.join(nc, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nc, "lib")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -14,6 +14,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -70,7 +72,9 @@ struct sor_grid {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   int halo_valid = kRowPad;  // rows of the current plane's halos known up to date
-  std::vector<std::pair<int64_t, std::pair<int, int>>> pass_ends;  // (last iteration, (cur after, T))
+  std::vector<std::pair<int64_t, std::pair<int, int>>> pass_ends;
+  // wave-kernel tile tables per (slab, T, occupancy): device int4 array + count
+  std::map<std::tuple<int, int, int>, std::pair<int4*, int>> tiles;  // (last iteration, (cur after, T))
   bool failed = false;
   bool have_elapsed = false;
   double elapsed_ms = 0.0;
@@ -239,6 +243,7 @@ void free_grid(sor_grid* g) {
     if (g->poll_ev[k]) cudaEventDestroy(g->poll_ev[k]);
   if (g->own_stream) cudaStreamDestroy(g->own_stream);
   if (g->comm) ncclCommDestroy(g->comm);
+  for (auto& kv : g->tiles) cudaFree(kv.second.first);
   delete g;
 }
 
@@ -460,6 +465,101 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
 template <typename R>
 constexpr int wave_nst() { return 12; }
 
+// ------------------------------------------------------------------ tiles
+// One warp per tile = (strip, band of owned rows).  A tile costs about
+// (rows + 4T-2 warm-up steps) x (alpha if it must keep ring/padding cells
+// fixed, "masked", else 1).  Short bands waste the 4T-2 ghost rows, one
+// partial extra wave doubles the tail, and in one long wave the slowest warp
+// sets the time.  So: if one wave of resident warps gives bands <= 512 rows,
+// use exactly one wave with band heights chosen so every tile costs about the
+// same (masked tiles get shorter bands, alpha = 1.7 measured on C3);
+// otherwise ~8 waves of bands >= 256 rows in row-major order.
+static bool tile_masked(const sor_grid* g, int T, int s0, int strip, int64_t R0, int64_t R1) {
+  const int64_t sw = s0 + (int64_t)strip * (kWaveCols - 4 * T);
+  const int64_t i_first = (R0 - (2 * T - 1)) & ~1LL;
+  const int64_t nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
+  return !((sw >= 1) && (sw + kWaveCols - 1 <= g->cols) && (i_first - 1 >= 1) &&
+           (i_first + nsteps <= g->rows));
+}
+
+int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
+               std::pair<int4*, int>* out) {
+  const auto key = std::make_tuple(slab_idx, T, occ);
+  auto it = g->tiles.find(key);
+  if (it != g->tiles.end()) {
+    *out = it->second;
+    return SOR_OK;
+  }
+  static double alpha = -1.0, waves = -1.0;
+  static int64_t min_h = 0;
+  if (alpha < 0) {
+    const char* e = getenv("SOR_WAVE_ALPHA");
+    alpha = e ? atof(e) : 1.7;
+    if (!(alpha >= 1.0)) alpha = 1.7;
+    e = getenv("SOR_WAVE_WAVES");
+    waves = e ? atof(e) : 0.0;  // 0 = automatic
+    e = getenv("SOR_WAVE_MIN_BAND");
+    min_h = e ? atoll(e) : 0;
+  }
+  const int64_t wout = kWaveCols - 4 * T;
+  const int nstrips = (int)((g->cols + 1 - (s0 + 2 * T) + wout - 1) / wout);
+  const int64_t nrows = s.g_hi - s.g_lo;
+  const int64_t slots = (int64_t)g->nsm * occ * kWaveWarps;
+  const int64_t warm = 4 * T - 2;
+  // split strip `w` given the target cost per tile (in row-steps)
+  auto split = [&](int w, double cost, std::vector<int4>* tl) {
+    int64_t r = s.g_lo;
+    while (r < s.g_hi) {
+      // try an unmasked-height band first; fall back to the masked height
+      int64_t h = std::max<int64_t>(8, (int64_t)(cost - warm));
+      bool m = tile_masked(g, T, s0, w, r, std::min(r + h, s.g_hi));
+      if (m) h = std::max<int64_t>(8, (int64_t)(cost / alpha - warm));
+      h = std::min<int64_t>(h, s.g_hi - r);
+      if (tl) tl->push_back(make_int4(w, (int)r, (int)(r + h), tile_masked(g, T, s0, w, r, r + h) ? 1 : 0));
+      r += h;
+    }
+  };
+  auto count = [&](double cost) {
+    std::vector<int4> tl;
+    for (int w = 0; w < nstrips; ++w) split(w, cost, &tl);
+    return (int64_t)tl.size();
+  };
+  double cost;
+  if (waves > 0) {
+    const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / nstrips);
+    cost = (double)std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb) + warm;
+  } else {
+    // smallest cost (shortest bands) that still fits one wave
+    double lo = 8 + warm, hi = (double)nrows + warm + 1;
+    if (count(hi) > slots) {
+      lo = hi;  // even whole-strip bands exceed a wave: many waves
+    } else {
+      for (int iter = 0; iter < 40; ++iter) {
+        const double mid = 0.5 * (lo + hi);
+        if (count(mid) <= slots) hi = mid; else lo = mid;
+      }
+    }
+    cost = hi;
+    const int64_t kOneWaveMaxH = 512, kMinH = min_h > 0 ? min_h : 256;
+    if (cost - warm > kOneWaveMaxH) {
+      const int64_t nb8 = std::max<int64_t>(1, 8 * slots / nstrips);
+      cost = (double)std::max<int64_t>(kMinH, (nrows + nb8 - 1) / nb8) + warm;
+    }
+  }
+  std::vector<int4> tl;
+  for (int w = 0; w < nstrips; ++w) split(w, cost, &tl);
+  // row-major order: warps running together stream neighbouring strips of the
+  // same rows (shared ghost columns hit in L2, DRAM pages stay open)
+  std::stable_sort(tl.begin(), tl.end(),
+                   [](const int4& x, const int4& y) { return x.y != y.y ? x.y < y.y : x.x < y.x; });
+  int4* d = nullptr;
+  CU(cudaMalloc(&d, tl.size() * sizeof(int4)));
+  CU(cudaMemcpy(d, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  *out = {d, (int)tl.size()};
+  g->tiles[key] = *out;
+  return SOR_OK;
+}
+
 template <typename R, int T, int CK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   constexpr int NST = wave_nst<R>();
@@ -481,48 +581,12 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
   a.r_hi = s.g_hi;
   a.w = w;
   a.s0 = -4 * ((2 * T + 3) / 4);
-  const int64_t wout = kWaveCols - 4 * T;
-  a.nstrips = (int)((g->cols + 1 - (a.s0 + 2 * T) + wout - 1) / wout);
-  const int64_t nrows = s.g_hi - s.g_lo;
-  // Tiles.  Short bands waste 4T-2 ghost rows each, one partial extra wave
-  // doubles the tail, and in a single long wave the slowest warp sets the
-  // time.  So: exactly one wave when that gives bands <= kOneWaveMaxH rows,
-  // otherwise ~8 waves of bands >= kMinH rows (dynamic load balance).
-  static double waves = -1.0;
-  static int64_t min_h = 0;
-  if (waves < 0) {
-    const char* e = getenv("SOR_WAVE_WAVES");
-    waves = e ? atof(e) : 0.0;  // 0 = automatic
-    const char* h = getenv("SOR_WAVE_MIN_BAND");
-    min_h = h ? atoll(h) : 0;
-  }
-  const int64_t slots = (int64_t)g->nsm * occ * kWaveWarps;
-  auto fit = [](int64_t bh, int T_) {  // even, and bh + 4T - 2 steps a multiple of 6
-    while ((bh & 1) || (bh + 4 * T_ - 2) % 6) ++bh;
-    return bh;
-  };
-  int64_t bh;
-  if (waves > 0) {
-    const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / a.nstrips);
-    bh = std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb);
-  } else {
-    const int64_t nb1 = std::max<int64_t>(1, slots / a.nstrips);  // bands in one wave
-    int64_t bh1 = fit((nrows + nb1 - 1) / nb1, T);
-    while (a.nstrips * ((nrows + bh1 - 1) / bh1) > slots) bh1 = fit(bh1 + 1, T);
-    const int64_t kOneWaveMaxH = 512, kMinH = min_h > 0 ? min_h : 256;
-    if (bh1 <= kOneWaveMaxH) {
-      bh = bh1;
-    } else {
-      const int64_t nb8 = std::max<int64_t>(1, 8 * slots / a.nstrips);
-      bh = std::max<int64_t>(kMinH, (nrows + nb8 - 1) / nb8);
-    }
-  }
-  bh = fit(bh, T);
-  int64_t nbands = (nrows + bh - 1) / bh;
-  a.band_h = bh;
-  a.nbands = (int)nbands;
-  const int64_t warps = (int64_t)a.nstrips * a.nbands;
-  const unsigned blocks = (unsigned)((warps + kWaveWarps - 1) / kWaveWarps);
+  const int slab_idx = (int)(&s - &g->slabs[0]);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, slab_idx, T, occ, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  const unsigned blocks = (unsigned)((a.ntiles + kWaveWarps - 1) / kWaveWarps);
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks;

@@ -235,8 +235,8 @@ struct WaveArgs {
   long long g0;      // global row of storage row 0
   long long rows, cols;
   long long r_lo, r_hi;  // owned global rows written by this launch
-  long long band_h;
-  int nstrips, nbands;
+  const int4* tiles;  // per warp: (strip, R0, R1, masked) — see launch_wave_T
+  int ntiles;
   int s0;            // first column of strip 0 (multiple of 4)
   R w;
 };
@@ -596,18 +596,22 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kern
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWaveWarps + warp;
   unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
-  if (gw < a.nstrips * a.nbands) {
-    const int strip = gw % a.nstrips;
-    const int band = gw / a.nstrips;
-    const int sw = a.s0 + strip * (kWaveCols - 4 * T);
-    const int R0 = (int)a.r_lo + band * (int)a.band_h;
-    const int R1 = min(R0 + (int)a.band_h, (int)a.r_hi);
+  if (gw < a.ntiles) {
+    const int4 tile = a.tiles[gw];
+    const int sw = a.s0 + tile.x * (kWaveCols - 4 * T);
+    const int R0 = tile.y;
+    const int R1 = tile.z;
     // step m (front row i_first+m) feeds stage 2T-1 row i_first+m-2T+1;
     // i_first even; nsteps a multiple of 6 (ring phase x parity)
     const int i_first = (R0 - (2 * T - 1)) & ~1;
     const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
-    const bool interior = (sw >= 1) && (sw + kWaveCols - 1 <= (int)a.cols) && (i_first - 1 >= 1) &&
-                          (i_first + nsteps <= (int)a.rows);
+#ifdef SOR_EXPERIMENT_FORCE_UNMASKED  // timing experiments only: wrong results at the edges
+    const bool interior = true;
+#else
+    // the host's classification (tile.w) is re-derived here as a safety net
+    const bool interior = !tile.w && (sw >= 1) && (sw + kWaveCols - 1 <= (int)a.cols) &&
+                          (i_first - 1 >= 1) && (i_first + nsteps <= (int)a.rows);
+#endif
     unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
     if (interior)
       wave_tile<R, T, NST, CK, false>(a, wbase, lane, sw, R0, R1, i_first, nsteps, dm);
