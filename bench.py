@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--kernel", default="temporal")
-    ap.add_argument("--T", type=int, default=3)
+    ap.add_argument("--T", type=int, default=4)
     ap.add_argument("--no-solve", action="store_true", help="fixed iterations only")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-iters", type=int, default=32)

@@ -154,6 +154,7 @@ typedef struct {
   int32_t rank, nranks;
   int64_t row_lo, row_hi;   /* owned global interior rows [row_lo, row_hi) of slab 0  */
   int64_t pitch_elems;      /* device row pitch in elements                           */
+  int64_t exact_reruns;     /* solve: passes re-run to decide the stop test exactly    */
 } sor_stats;
 int sor_get_stats(const sor_grid* g, sor_stats* out);
 

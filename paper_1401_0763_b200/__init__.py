@@ -45,7 +45,7 @@ class Stats(ctypes.Structure):
                 ("temporal_depth", ctypes.c_int32), ("nslabs", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("row_lo", ctypes.c_int64), ("row_hi", ctypes.c_int64),
-                ("pitch_elems", ctypes.c_int64)]
+                ("pitch_elems", ctypes.c_int64), ("exact_reruns", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -75,6 +75,8 @@ struct sor_grid {
   std::vector<std::pair<int64_t, std::pair<int, int>>> pass_ends;
   // wave-kernel tile tables per (slab, T, occupancy): device int4 array + count
   std::map<std::tuple<int, int, int>, std::pair<int4*, int>> tiles;  // (last iteration, (cur after, T))
+  int64_t exact_reruns = 0;  // solve passes re-run with exact maxima (diagnostic)
+  int every_ck = 4;          // max-change mode of T-deep solve passes with check_every == 1
   bool failed = false;
   bool have_elapsed = false;
   double elapsed_ms = 0.0;
@@ -598,7 +600,7 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
 
 template <typename R, int CK>
 int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool fused_fin) {
-  if (CK == 3 && T == 1) return launch_wave_T<R, 1, 2>(g, s, w, ctl, fused_fin);  // unused combination
+  if (CK >= 3 && T == 1) return launch_wave_T<R, 1, 2>(g, s, w, ctl, fused_fin);  // unused combination
   switch (T) {
     case 1: return launch_wave_T<R, 1, CK>(g, s, w, ctl, fused_fin);
     case 2: return launch_wave_T<R, 2, CK>(g, s, w, ctl, fused_fin);
@@ -615,7 +617,9 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   const bool fused_fin = single_part(g) && ctl.ck != 0;
   if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
   for (auto& s : g->slabs) {
-    if (ctl.ck == 3)
+    if (ctl.ck == 4)
+      TRY((launch_wave<R, 4>(g, s, T, w, ctl, fused_fin)));
+    else if (ctl.ck == 3)
       TRY((launch_wave<R, 3>(g, s, T, w, ctl, fused_fin)));
     else if (ctl.ck == 2)
       TRY((launch_wave<R, 2>(g, s, T, w, ctl, fused_fin)));
@@ -659,6 +663,8 @@ int begin_call(sor_grid* g) {
   g->st.hbm_passes = 0;
   g->have_elapsed = false;
   g->pass_ends.clear();
+  g->exact_reruns = 0;
+  g->st.exact_reruns = 0;
   CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
   CU(cudaEventRecord(g->ev0, g->stream));
   return SOR_OK;
@@ -677,6 +683,19 @@ int end_call(sor_grid* g, DevState* out) {
 }
 
 int depth_of(const sor_grid* g) { return g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1; }
+
+// Max-change mode of T-deep solve passes with check_every == 1: 4 (probe
+// rows) or 3 (all cells, high words).  Measured on C3 (B200): ck=4 wins for
+// T=4, ck=3 for T<=3.  SOR_SOLVE_CK=3|4 overrides.
+int solve_ck(int T) {
+  static int ck = -1;
+  if (ck < 0) {
+    const char* e = getenv("SOR_SOLVE_CK");
+    ck = e ? atoi(e) : 0;
+  }
+  if (ck == 3 || ck == 4) return ck;
+  return T >= 4 ? 4 : 3;
+}
 
 // Enqueue iterations [k_from, k_to] (1-based within the call).
 //  - iterate (base.solve == 0): passes of up to T; the last one reports its
@@ -715,7 +734,7 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
       IterCtl c = base;
       c.k_last = k + t - 1;
       c.T = t;
-      c.ck = every ? 3 : (c.k_last == next_check ? 1 : 0);
+      c.ck = every ? g->every_ck : (c.k_last == next_check ? 1 : 0);
       TRY(wave_pass<R>(g, w, c));
       if (c.ck) g->st.checks += every ? t : 1;
       k += t;
@@ -814,12 +833,16 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
       memcpy(&tb, &tol, 8);
       base.tol_hi = (unsigned)(tb >> 32);
     }
-    const bool fast = g->kernel != SOR_KERNEL_NATURAL && K == 1 && depth_of(g) > 1;  // ck=3 passes
+    const bool fast = g->kernel != SOR_KERNEL_NATURAL && K == 1 && depth_of(g) > 1;  // ck=3/4 passes
     // batches of whole check blocks (and whole passes); poll one batch behind
     const int64_t unit = std::max<int64_t>(K, depth_of(g));
     const int64_t blk = std::max<int64_t>(unit, (int64_t)((64 + unit - 1) / unit) * unit);
     int64_t k = 1;
     int64_t checks = 0;
+    // far from convergence the probe (ck=4) proves "not converged" at 1/6 of
+    // the max-change cost; after its first inconclusive pass the solve is
+    // near the end and switches to all cells (ck=3) to avoid repeated re-runs
+    g->every_ck = solve_ck(depth_of(g));
     while (true) {
       // one segment: iterations k..maxit until the device stops the loop
       CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
@@ -849,7 +872,10 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
       int64_t k_end = 0;
       int cur_after = g->cur, tp = 1;
       if (hs.ambiguous) {
-        // high words tied with tol's: decide this pass exactly
+        // ck=3: high words tied with tol's; ck=4: the probe could not exclude
+        // convergence.  Decide this pass exactly
+        g->exact_reruns += 1;
+        if (getenv("SOR_DEBUG")) fprintf(stderr, "[sor] exact re-run at iteration %lld\n", (long long)hs.amb_iter);
         if (!find_pass(g, hs.amb_iter, &k_end, &cur_after, &tp))
           return set_error(g, SOR_E_STATE, "internal: pass of iteration %lld not found", (long long)hs.amb_iter);
         checks -= (hs.amb_iter - (k_end - tp + 1)) + 1;  // the exact pass re-counts them
@@ -867,6 +893,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         }
         checks += ex.checks;
         maxc = ex.max_change;
+        g->every_ck = 3;
         k = k_end + 1;  // g->cur now holds X_{k_end}
         if (k > maxit) {
           done = maxit;
@@ -895,6 +922,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     }
     TRY(end_call(g, &hs));
     g->st.checks = checks;
+    g->st.exact_reruns = g->exact_reruns;
   }
   g->st.half_sweeps = 2 * done;
   if (iters_out) *iters_out = converged ? done : maxit;

@@ -66,7 +66,9 @@ struct IterCtl {
   int T;                // iterations in this pass
   int ck;               // 0: no max-change; 1: exact, of iteration k_last; 2: exact, of every
                         // iteration; 3: high 32 bits only, of every iteration (stop decision
-                        // exact unless the high words tie with tol's -> ambiguous)
+                        // exact unless the high words tie with tol's -> ambiguous); 4: as 3 on
+                        // a probe subset (1/6 of the rows): a lower bound, so "probe >= tol"
+                        // proves "not converged" and anything else is resolved exactly
   unsigned int tol_hi;  // high 32 bits of tol (ck=3)
   int solve;            // apply the stop test / early exit
   int finalize;         // this launch's last part runs the stop test
@@ -127,13 +129,23 @@ __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) 
     const int slot = every ? t : 0;
     const bool checked = every ? (!ctl.solve || k % ctl.K == 0) : (t == ctl.T - 1);
     if (!checked) continue;
-    if (ctl.ck == 3) {
+    if (ctl.ck >= 3) {
       // non-negative doubles order like their bit patterns: a smaller high
       // word decides '<', a larger one '>='; equal high words are ambiguous
       const unsigned int h = (unsigned int)(st->maxbits[slot][0] >> 32);
       st->checks += 1;
       st->iters_done = k;
       st->max_change = __longlong_as_double((long long)((unsigned long long)h << 32));
+      if (ctl.ck == 4) {
+        // probe max <= full max: only "probe > tol" is conclusive
+        if (h <= ctl.tol_hi) {
+          st->ambiguous = 1;
+          st->amb_iter = k;
+          st->stop = 1;
+          break;
+        }
+        continue;
+      }
       if (h < ctl.tol_hi) {
         st->converged = 1;
         st->conv_iter = k;
@@ -385,6 +397,9 @@ template <typename R, int T, int NST, int CK, bool MASK>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
   static constexpr int NSLOT = CK >= 2 ? T : 1;
+  // CK 4 probes the rows with (row - i_first) % 6 == 0: in the 6-step
+  // unrolled loop that is the compile-time condition (M6 - s) % 6 == 0
+  __host__ __device__ static constexpr bool probe_row(int M6, int s) { return ((M6 - s) % 6 + 6) % 6 == 0; }
   R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3
   R C[S - 1][3][2];           // stage outputs, slot = step % 3
   unsigned long long dmax[NSLOT];   // CK 1, 2: ordered bits; CK 3: high word in the low half
@@ -459,7 +474,7 @@ struct WavePipe {
         v0 = (rowok && upd[O]) ? v0 : u0;
         v1 = (rowok && upd[O + 2]) ? v1 : u1;
       }
-      if (CK == 3) {
+      if (CK == 3 || (CK == 4 && probe_row(M6, s))) {
         const bool inb = (r >= R0) & (r < R1);
         const unsigned int mA = inb ? ownA : 0u, mB = inb ? ownB : 0u;
         const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & mA;
@@ -586,7 +601,10 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
 }
 
 // Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines.
-__host__ __device__ constexpr int wave_min_blocks(int T) { return T <= 2 ? 4 : 3; }
+#ifndef SOR_WAVE_MINB34
+#define SOR_WAVE_MINB34 3
+#endif
+__host__ __device__ constexpr int wave_min_blocks(int T) { return T <= 2 ? 4 : SOR_WAVE_MINB34; }
 
 template <typename R, int T, int NST, int CK>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
@@ -625,7 +643,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kern
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
       const unsigned long long m =
-          CK == 3 ? ((unsigned long long)__reduce_max_sync(0xffffffffu, (unsigned int)dm[t]) << 32)
+          CK >= 3 ? ((unsigned long long)__reduce_max_sync(0xffffffffu, (unsigned int)dm[t]) << 32)
                   : warp_max_u64(dm[t]);
       if (lane == 0) cta_max[warp][t] = m;
     }

@@ -19,4 +19,4 @@ for kernel, T in (("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4
         st = g.stats
         print(f"{kernel:9s} T={T}: iterate {cfg.iters} in {t_it:8.2f} ms ({cfg.rows*cfg.cols*cfg.iters/t_it/1e6:7.1f} GLUP/s); "
               f"solve {r.iters} its conv={r.converged} max={r.max_change:.4e} in {t_s:8.2f} ms "
-              f"({cfg.rows*cfg.cols*r.iters/t_s/1e6:7.1f} GLUP/s) launches={st['kernel_launches']}", flush=True)
+              f"({cfg.rows*cfg.cols*r.iters/t_s/1e6:7.1f} GLUP/s) launches={st['kernel_launches']} reruns={st['exact_reruns']}", flush=True)
