@@ -685,16 +685,16 @@ int end_call(sor_grid* g, DevState* out) {
 int depth_of(const sor_grid* g) { return g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1; }
 
 // Max-change mode of T-deep solve passes with check_every == 1: 4 (probe
-// rows) or 3 (all cells, high words).  Measured on C3 (B200): ck=4 wins for
-// T=4, ck=3 for T<=3.  SOR_SOLVE_CK=3|4 overrides.
+// rows, default: 1.09-1.23x the cost of a plain pass on C3 vs 1.10-1.41x for
+// all cells) or 3 (all cells, high words).  SOR_SOLVE_CK=3 overrides.
 int solve_ck(int T) {
   static int ck = -1;
   if (ck < 0) {
     const char* e = getenv("SOR_SOLVE_CK");
     ck = e ? atoi(e) : 0;
   }
-  if (ck == 3 || ck == 4) return ck;
-  return T >= 4 ? 4 : 3;
+  (void)T;
+  return ck == 3 ? 3 : 4;
 }
 
 // Enqueue iterations [k_from, k_to] (1-based within the call).
@@ -893,7 +893,10 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         }
         checks += ex.checks;
         maxc = ex.max_change;
-        g->every_ck = 3;
+        // near convergence (exact max within 16x tol) probing would keep
+        // failing: switch to all cells.  Far from it (e.g. a probe that saw
+        // only still-unchanged rows) keep probing.
+        if (ex.max_change < 16.0 * tol) g->every_ck = 3;
         k = k_end + 1;  // g->cur now holds X_{k_end}
         if (k > maxit) {
           done = maxit;

@@ -402,7 +402,8 @@ struct WavePipe {
   __host__ __device__ static constexpr bool probe_row(int M6, int s) { return ((M6 - s) % 6 + 6) % 6 == 0; }
   R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3
   R C[S - 1][3][2];           // stage outputs, slot = step % 3
-  unsigned long long dmax[NSLOT];   // CK 1, 2: ordered bits; CK 3: high word in the low half
+  unsigned long long dmax[CK == 1 || CK == 2 ? NSLOT : 1];  // CK 1, 2: ordered bits
+  unsigned int hmax[CK >= 3 ? NSLOT : 1];                     // CK 3, 4: high words
   unsigned int ownA, ownB;         // CK 3: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
   bool upd[4], own[4];
   bool own_all;
@@ -440,6 +441,12 @@ struct WavePipe {
     constexpr int P1 = (PH + 2) % 3;    // age 1
     constexpr int P2 = (PH + 1) % 3;    // age 2
     lds4(rowp + M6 * kWaveCols, F[P1]); // source row i+1 (ring slot (m+2)%3)
+    // CK 3/4: bit s set iff stage s's row i-s is owned (R0 <= i-s < R1)
+    unsigned int rowm = 0u;
+    if (CK >= 3) {
+      const int lo_s = max(0, i - R1 + 1), hi_s = min(S - 1, i - R0);
+      rowm = hi_s >= lo_s ? (((2u << hi_s) - 1u) & ~((1u << lo_s) - 1u)) : 0u;
+    }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int r = i - s;
@@ -475,12 +482,11 @@ struct WavePipe {
         v1 = (rowok && upd[O + 2]) ? v1 : u1;
       }
       if (CK == 3 || (CK == 4 && probe_row(M6, s))) {
-        const bool inb = (r >= R0) & (r < R1);
-        const unsigned int mA = inb ? ownA : 0u, mB = inb ? ownB : 0u;
-        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & mA;
-        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & mB;
-        const int slot = s >> 1;
-        dmax[slot] = max3u((unsigned int)dmax[slot], hA, hB);
+        // all-ones iff this stage's row is an owned row (bit s of rowm)
+        const unsigned int fill = (unsigned int)((int)(rowm << (31 - s)) >> 31);
+        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & ownA & fill;
+        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & ownB & fill;
+        hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
       } else if (CK != 0 && (CK == 2 || s >= S - 2)) {
         const bool inb = (r >= R0) & (r < R1);
         const int slot = CK == 2 ? (s >> 1) : 0;
@@ -538,7 +544,10 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
                                           unsigned long long (&dm)[kMaxT]) {
   WavePipe<R, T, NST, CK, MASK> P;
 #pragma unroll
-  for (int t = 0; t < P.NSLOT; ++t) P.dmax[t] = 0ull;
+  for (int t = 0; t < P.NSLOT; ++t) {
+    if (CK == 1 || CK == 2) P.dmax[t] = 0ull;
+    if (CK >= 3) P.hmax[t] = 0u;
+  }
   P.ring = reinterpret_cast<const R*>(wbase);
   P.ring_s = smem_u32(wbase);
   P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
@@ -597,7 +606,7 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
   }
   P.run(a, i_first, c0);
 #pragma unroll
-  for (int t = 0; t < P.NSLOT; ++t) dm[t] = P.dmax[t];
+  for (int t = 0; t < P.NSLOT; ++t) dm[t] = CK >= 3 ? (unsigned long long)P.hmax[t] : P.dmax[(CK == 1 || CK == 2) ? t : 0];
 }
 
 // Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines.

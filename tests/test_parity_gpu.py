@@ -234,3 +234,22 @@ def test_solve_high_word_tie_resolved_exactly(gpu, orc, T, nudge):
         out = g.download()
     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("kernel,T", [("fused", 1), ("temporal", 3), ("natural", 1)])
+def test_dist_single_rank_nccl(gpu, orc, kernel, T):
+    """sor_create_dist with nranks=1: NCCL communicator, allreduce-max + finalize path."""
+    init = SI.random_edges(90, 130, seed=31)
+    ref = init.copy()
+    orc.iterate(ref, 1.7, 10)
+    rr = orc.solve(ref, 1.7, 1e-4, 3000, 2)
+    uid = gpu.nccl_unique_id()
+    with gpu.Grid.create_dist(init, 0, 1, 0, uid) as g:
+        g.set_kernel(kernel, T)
+        g.iterate(1.7, 10)
+        r = g.solve(1.7, 1e-4, 3000, 2)
+        out = g.download()
+        st = g.stats
+    assert (st["rank"], st["nranks"]) == (0, 1)
+    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
+    assert np.array_equal(out, ref)
