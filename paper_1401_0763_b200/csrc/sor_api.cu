@@ -484,9 +484,9 @@ static bool tile_masked(const sor_grid* g, int T, int s0, int strip, int64_t R0,
            (i_first + nsteps <= g->rows));
 }
 
-int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
+int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm, bool split, int s0,
                std::pair<int4*, int>* out) {
-  const auto key = std::make_tuple(slab_idx, T, occ);
+  const auto key = std::make_tuple(slab_idx, T * 2 + (split ? 1 : 0), tiles_per_sm);
   auto it = g->tiles.find(key);
   if (it != g->tiles.end()) {
     *out = it->second;
@@ -506,10 +506,10 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
   const int64_t wout = kWaveCols - 4 * T;
   const int nstrips = (int)((g->cols + 1 - (s0 + 2 * T) + wout - 1) / wout);
   const int64_t nrows = s.g_hi - s.g_lo;
-  const int64_t slots = (int64_t)g->nsm * occ * kWaveWarps;
+  const int64_t slots = (int64_t)g->nsm * tiles_per_sm;
   const int64_t warm = 4 * T - 2;
   // split strip `w` given the target cost per tile (in row-steps)
-  auto split = [&](int w, double cost, std::vector<int4>* tl) {
+  auto split_strip = [&](int w, double cost, std::vector<int4>* tl) {
     int64_t r = s.g_lo;
     while (r < s.g_hi) {
       // try an unmasked-height band first; fall back to the masked height
@@ -523,7 +523,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
   };
   auto count = [&](double cost) {
     std::vector<int4> tl;
-    for (int w = 0; w < nstrips; ++w) split(w, cost, &tl);
+    for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
     return (int64_t)tl.size();
   };
   double cost;
@@ -549,7 +549,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
     }
   }
   std::vector<int4> tl;
-  for (int w = 0; w < nstrips; ++w) split(w, cost, &tl);
+  for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
   // row-major order: warps running together stream neighbouring strips of the
   // same rows (shared ghost columns hit in L2, DRAM pages stay open)
   std::stable_sort(tl.begin(), tl.end(),
@@ -562,14 +562,26 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int occ, int s0,
   return SOR_OK;
 }
 
-template <typename R, int T, int CK>
-int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+// Split mode (a warp pair per tile, stages divided between the two warps) for
+// T >= 2 unless SOR_WAVE_SPLIT=0.
+bool wave_split(int T) {
+  static int sp = -1;
+  if (sp < 0) {
+    const char* e = getenv("SOR_WAVE_SPLIT");
+    sp = e ? atoi(e) : 1;
+  }
+  return sp != 0 && T >= 2;
+}
+
+template <typename R, int T, int CK, bool SPLIT>
+int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   constexpr int NST = wave_nst<R>();
-  constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST>();
+  constexpr int smem = wave_smem_bytes<R, NST, SPLIT>();
+  constexpr int per_cta = wave_tiles_per_cta(SPLIT);
   static int occ = 0;  // resident CTAs/SM for this instance
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -585,17 +597,23 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
   a.s0 = -4 * ((2 * T + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, T, occ, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, T, occ * per_cta, SPLIT, a.s0, &tt));
   a.tiles = tt.first;
   a.ntiles = tt.second;
-  const unsigned blocks = (unsigned)((a.ntiles + kWaveWarps - 1) / kWaveWarps);
+  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta);
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks;
-  wave_kernel<R, T, NST, CK><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
+  wave_kernel<R, T, NST, CK, SPLIT><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
   return SOR_OK;
+}
+
+template <typename R, int T, int CK>
+int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  if (T >= 2 && wave_split(T)) return launch_wave_TS<R, T, CK, (T >= 2)>(g, s, w, ctl, fused_fin);
+  return launch_wave_TS<R, T, CK, false>(g, s, w, ctl, fused_fin);
 }
 
 template <typename R, int CK>

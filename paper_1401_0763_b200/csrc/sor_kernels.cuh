@@ -352,6 +352,19 @@ template <typename R, int NST>
 __host__ __device__ constexpr int wave_smem_per_warp() {
   return (NST * kWaveCols * (int)sizeof(R) + 3 * 8 + 127) / 128 * 128;  // 128-B aligned bases
 }
+// Split mode: a warp PAIR shares one tile.  The front warp streams the source
+// and runs stages [0, T), the back warp runs stages [T, 2T); per step the
+// front hands over its last two stages' outputs (4 values per lane) through a
+// 2-batch shared ring synchronised with named barriers.  Half the registers
+// per warp -> twice the resident warps, and no spills at T = 4.
+template <typename R>
+__host__ __device__ constexpr int wave_handoff_bytes() {
+  return 2 * 6 * 32 * 4 * (int)sizeof(R);  // 2 batches x 6 steps x 32 lanes x 4 values
+}
+template <typename R, int NST>
+__host__ __device__ constexpr int wave_smem_per_pair() {
+  return wave_smem_per_warp<R, NST>() + wave_handoff_bytes<R>();
+}
 
 // Predicated stores (branch-free, so unrolled steps form one basic block).
 __device__ __forceinline__ void stg4_if(bool p, double* a, const double (&x)[4]) {
@@ -374,6 +387,12 @@ __device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
                "r"((int)p)
                : "memory");
 }
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 // Register pipeline of one warp.
 //
@@ -387,24 +406,28 @@ __device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
 // no value is ever moved.  Source rows arrive through an NST-deep shared
 // ring filled by TMA bulk copies issued NST rows ahead.
 //
+// This warp runs stages [SB, SE) of the S = 2T stages: SB == 0 streams the
+// source; SB > 0 receives stages SB-1, SB-2 from the front warp; SE < S hands
+// stages SE-1, SE-2 on; SE == S writes finished rows.
+//
 // CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each,
 // 3 = high 32 bits of |delta| of each (VIMNMX3, ~1.5 ALU ops per cell).
 // MASK: false for warps whose rows and columns are all interior cells (no
 // Dirichlet/padding cell to keep fixed).  Ownership (which computed cells
 // are valid and written: the strip minus its 2T ghost columns on each side,
 // the band's rows) applies to every warp.
-template <typename R, int T, int NST, int CK, bool MASK>
+template <typename R, int T, int NST, int CK, bool MASK, int SB, int SE>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
   static constexpr int NSLOT = CK >= 2 ? T : 1;
   // CK 4 probes the rows with (row - i_first) % 6 == 0: in the 6-step
   // unrolled loop that is the compile-time condition (M6 - s) % 6 == 0
   __host__ __device__ static constexpr bool probe_row(int M6, int s) { return ((M6 - s) % 6 + 6) % 6 == 0; }
-  R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3
-  R C[S - 1][3][2];           // stage outputs, slot = step % 3
+  R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3 (front warp)
+  R C[S - 1][3][2];           // stage outputs, slot = step % 3 (unused stages vanish)
   unsigned long long dmax[CK == 1 || CK == 2 ? NSLOT : 1];  // CK 1, 2: ordered bits
   unsigned int hmax[CK >= 3 ? NSLOT : 1];                     // CK 3, 4: high words
-  unsigned int ownA, ownB;         // CK 3: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
+  unsigned int ownA, ownB;         // CK 3/4: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
   bool upd[4], own[4];
   bool own_all;
   int rows, R0, R1;
@@ -416,6 +439,8 @@ struct WavePipe {
   long long pitch;
   int nbatch;
   int lane;
+  R* hand;                    // split: handoff ring [2][6][32][4]
+  int bar_full, bar_empty;    // split: named barrier ids (+ batch parity)
   static constexpr uint32_t ROWB = kWaveCols * sizeof(R);
 
   // lane 0: rows k_lo..k_hi-1 of batch j (expect_tx covers the whole batch
@@ -435,12 +460,22 @@ struct WavePipe {
   }
 
   template <int M6>
-  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, long long c0) {
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, R* hp, long long c0) {
     constexpr int O = M6 & 1;
     constexpr int PH = M6 % 3;          // slot of age 0 (this step)
     constexpr int P1 = (PH + 2) % 3;    // age 1
     constexpr int P2 = (PH + 1) % 3;    // age 2
-    lds4(rowp + M6 * kWaveCols, F[P1]); // source row i+1 (ring slot (m+2)%3)
+    if (SB == 0) {
+      lds4(rowp + M6 * kWaveCols, F[P1]);  // source row i+1 (ring slot (m+2)%3)
+    } else {
+      // stages SB-1 (row i-SB+1) and SB-2 (row i-SB+2) of this step, from the front warp
+      R x[4];
+      lds4(hp + (M6 * 32 + lane) * 4, x);
+      C[SB - 1][PH][0] = x[0];
+      C[SB - 1][PH][1] = x[1];
+      C[SB - 2][PH][0] = x[2];
+      C[SB - 2][PH][1] = x[3];
+    }
     // CK 3/4: bit s set iff stage s's row i-s is owned (R0 <= i-s < R1)
     unsigned int rowm = 0u;
     if (CK >= 3) {
@@ -448,7 +483,7 @@ struct WavePipe {
       rowm = hi_s >= lo_s ? (((2u << hi_s) - 1u) & ~((1u << lo_s) - 1u)) : 0u;
     }
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
+    for (int s = SB; s < SE; ++s) {
       const int r = i - s;
       R n0, n1, s0, s1, w0, w1, u0, u1;
       if (s == 0) {
@@ -514,35 +549,63 @@ struct WavePipe {
         }
       }
     }
+    if (SE < S) {
+      R x[4] = {C[SE - 1][PH][0], C[SE - 1][PH][1], C[SE - 2][PH][0], C[SE - 2][PH][1]};
+      R* q = hp + (M6 * 32 + lane) * 4;
+      if (sizeof(R) == 8) {
+        reinterpret_cast<double2*>(q)[0] = make_double2((double)x[0], (double)x[1]);
+        reinterpret_cast<double2*>(q)[1] = make_double2((double)x[2], (double)x[3]);
+      } else {
+        *reinterpret_cast<float4*>(q) = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+      }
+    }
   }
 
   __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, long long c0) {
+    constexpr bool front = SB == 0, back = SE == S;
+    constexpr bool split = !(front && back);
+    if (split && !front) {  // back warp: both handoff buffers start empty
+      named_bar_arrive(bar_empty + 0, 64);
+      if (nbatch > 1) named_bar_arrive(bar_empty + 1, 64);
+    }
 #pragma unroll 1
     for (int j = 0; j < nbatch; ++j) {
       const int m = 6 * j;
-      mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
-      const R* rowp = ring + (j & 1) * 6 * kWaveCols + 4 * lane;
-      step<0>(a, i_first + m, rowp, c0);
-      step<1>(a, i_first + m + 1, rowp, c0);
-      step<2>(a, i_first + m + 2, rowp, c0);
-      step<3>(a, i_first + m + 3, rowp, c0);
-      step<4>(a, i_first + m + 4, rowp, c0);
-      step<5>(a, i_first + m + 5, rowp, c0);
-      __syncwarp();
-      if (lane == 0 && j + 2 < nbatch) {
-        fence_proxy_async_smem();  // our generic reads of the slots precede the async refill
-        issue_batch(j + 2);
+      const R* rowp = nullptr;
+      R* hp = split ? hand + (j & 1) * (6 * 32 * 4) : nullptr;
+      if (front) {
+        mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
+        rowp = ring + (j & 1) * 6 * kWaveCols + 4 * lane;
+        if (split) named_bar_sync(bar_empty + (j & 1), 64);
+      } else {
+        named_bar_sync(bar_full + (j & 1), 64);
+      }
+      step<0>(a, i_first + m, rowp, hp, c0);
+      step<1>(a, i_first + m + 1, rowp, hp, c0);
+      step<2>(a, i_first + m + 2, rowp, hp, c0);
+      step<3>(a, i_first + m + 3, rowp, hp, c0);
+      step<4>(a, i_first + m + 4, rowp, hp, c0);
+      step<5>(a, i_first + m + 5, rowp, hp, c0);
+      if (front) {
+        if (split) named_bar_arrive(bar_full + (j & 1), 64);
+        __syncwarp();
+        if (lane == 0 && j + 2 < nbatch) {
+          fence_proxy_async_smem();  // our generic reads of the slots precede the async refill
+          issue_batch(j + 2);
+        }
+      } else if (j + 2 < nbatch) {
+        named_bar_arrive(bar_empty + (j & 1), 64);
       }
     }
   }
 };
 
-// One warp = one (strip, band) tile; warps never synchronise with each other.
-template <typename R, int T, int NST, int CK, bool MASK>
-__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* wbase, int lane,
-                                          int sw, int R0, int R1, int i_first, int nsteps,
+// One warp (or warp pair) = one (strip, band) tile; tiles never synchronise.
+template <typename R, int T, int NST, int CK, bool MASK, int SB, int SE>
+__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* wbase, R* hand, int bar_id,
+                                          int lane, int sw, int R0, int R1, int i_first, int nsteps,
                                           unsigned long long (&dm)[kMaxT]) {
-  WavePipe<R, T, NST, CK, MASK> P;
+  WavePipe<R, T, NST, CK, MASK, SB, SE> P;
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) {
     if (CK == 1 || CK == 2) P.dmax[t] = 0ull;
@@ -552,6 +615,9 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
   P.ring_s = smem_u32(wbase);
   P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
   static_assert(NST == 12, "ring layout: 2 batches of 6 rows");
+  P.hand = hand;
+  P.bar_full = bar_id;
+  P.bar_empty = bar_id + 2;
   P.lane = lane;
   P.rows = (int)a.rows;
   P.R0 = R0;
@@ -585,43 +651,57 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
   P.pitch = a.pitch;
   P.gsrc = a.src + (long long)(i_first - 1 - a.g0) * a.pitch + sw;
   P.nbatch = nsteps / 6;
-  if (lane == 0) {
+  if (SB == 0) {
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) mbar_init(P.bar_s + 8u * k, 1u);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  if (lane == 0) {
-    P.issue_prologue();
-    P.issue_batch(0);
-    if (P.nbatch > 1) P.issue_batch(1, 0, 4);
-  }
-  mbar_wait(P.bar_s + 16u, 0u);
-  lds4(P.ring + 10 * kWaveCols + 4 * lane, P.F[0]);  // row i_first - 1
-  lds4(P.ring + 11 * kWaveCols + 4 * lane, P.F[1]);  // row i_first
-  __syncwarp();
-  if (lane == 0 && P.nbatch > 1) {
-    fence_proxy_async_smem();
-    P.issue_batch(1, 4, 6);
+      for (int k = 0; k < 3; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) {
+      P.issue_prologue();
+      P.issue_batch(0);
+      if (P.nbatch > 1) P.issue_batch(1, 0, 4);
+    }
+    mbar_wait(P.bar_s + 16u, 0u);
+    lds4(P.ring + 10 * kWaveCols + 4 * lane, P.F[0]);  // row i_first - 1
+    lds4(P.ring + 11 * kWaveCols + 4 * lane, P.F[1]);  // row i_first
+    __syncwarp();
+    if (lane == 0 && P.nbatch > 1) {
+      fence_proxy_async_smem();
+      P.issue_batch(1, 4, 6);
+    }
   }
   P.run(a, i_first, c0);
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) dm[t] = CK >= 3 ? (unsigned long long)P.hmax[t] : P.dmax[(CK == 1 || CK == 2) ? t : 0];
 }
 
-// Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines.
+// Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines;
+// split kernels hold half the stages per warp and aim for 4 CTAs.
 #ifndef SOR_WAVE_MINB34
 #define SOR_WAVE_MINB34 3
 #endif
-__host__ __device__ constexpr int wave_min_blocks(int T) { return T <= 2 ? 4 : SOR_WAVE_MINB34; }
+__host__ __device__ constexpr int wave_min_blocks(int T, bool split) {
+  return split ? 4 : (T <= 2 ? 4 : SOR_WAVE_MINB34);
+}
+// warps (tiles, or warp pairs in split mode) per CTA
+__host__ __device__ constexpr int wave_tiles_per_cta(bool split) { return split ? kWaveWarps / 2 : kWaveWarps; }
+template <typename R, int NST, bool SPLIT>
+__host__ __device__ constexpr int wave_smem_bytes() {
+  return SPLIT ? (kWaveWarps / 2) * wave_smem_per_pair<R, NST>() : kWaveWarps * wave_smem_per_warp<R, NST>();
+}
 
-template <typename R, int T, int NST, int CK>
-__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kernel(WaveArgs<R> a, IterCtl ctl) {
+template <typename R, int T, int NST, int CK, bool SPLIT>
+__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
+    wave_kernel(WaveArgs<R> a, IterCtl ctl) {
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
   extern __shared__ __align__(128) unsigned char wave_smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWaveWarps + warp;
+  const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
+  const int role = SPLIT ? warp & 1 : 0;      // 0 front (or whole), 1 back
+  const int gw = blockIdx.x * wave_tiles_per_cta(SPLIT) + slot;
   unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
   if (gw < a.ntiles) {
     const int4 tile = a.tiles[gw];
@@ -639,12 +719,30 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T)) wave_kern
     const bool interior = !tile.w && (sw >= 1) && (sw + kWaveCols - 1 <= (int)a.cols) &&
                           (i_first - 1 >= 1) && (i_first + nsteps <= (int)a.rows);
 #endif
-    unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
-    if (interior)
-      wave_tile<R, T, NST, CK, false>(a, wbase, lane, sw, R0, R1, i_first, nsteps, dm);
-    else
-      wave_tile<R, T, NST, CK, true>(a, wbase, lane, sw, R0, R1, i_first, nsteps, dm);
+    if (SPLIT) {
+      unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST>();
+      R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST>());
+      const int bar_id = 1 + 4 * slot;  // named barriers 1..8 (0 is __syncthreads)
+      if (role == 0) {
+        if (interior)
+          wave_tile<R, T, NST, CK, false, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        else
+          wave_tile<R, T, NST, CK, true, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+      } else {
+        if (interior)
+          wave_tile<R, T, NST, CK, false, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        else
+          wave_tile<R, T, NST, CK, true, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+      }
+    } else {
+      unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
+      if (interior)
+        wave_tile<R, T, NST, CK, false, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+      else
+        wave_tile<R, T, NST, CK, true, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+    }
   }
+  (void)role;
   if (CK != 0) {
     // warp max -> CTA max in shared memory -> one atomic per CTA and slot
     constexpr int NS = CK >= 2 ? T : 1;
