@@ -275,7 +275,7 @@ def main():
     solve_dominant = t_sv_total > t_it_total
     if solve_dominant:
         t_launch_ms = t_sv_total / sum(r["solve_launches"] for r in recs)
-        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck={3 if T_eff > 1 else 1}> (solve phase)"
+        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck={4 if T_eff > 1 else 1}> (solve phase)"
     else:
         t_launch_ms = t_it_total / sum(r["iterate_launches"] for r in recs)
         kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck=0> (fixed-iteration phase)"
