@@ -468,14 +468,13 @@ template <typename R>
 constexpr int wave_nst() { return 12; }
 
 // ------------------------------------------------------------------ tiles
-// One warp per tile = (strip, band of owned rows).  A tile costs about
-// (rows + 4T-2 warm-up steps) x (alpha if it must keep ring/padding cells
-// fixed, "masked", else 1).  Short bands waste the 4T-2 ghost rows, one
-// partial extra wave doubles the tail, and in one long wave the slowest warp
-// sets the time.  So: if one wave of resident warps gives bands <= 512 rows,
-// use exactly one wave with band heights chosen so every tile costs about the
-// same (masked tiles get shorter bands, alpha = 1.7 measured on C3);
-// otherwise ~8 waves of bands >= 256 rows in row-major order.
+// One warp (pair) per tile = (strip, band of owned rows).  A tile runs whole
+// 6-step batches and costs about its batch count x (alpha if it must keep
+// ring/padding cells fixed, "masked", else 1).  Short bands waste the 4T-2
+// warm-up steps and one partial extra wave doubles the tail, so if one wave of
+// resident tiles gives bands <= 512 rows the launch is exactly one wave with
+// batch counts equalised (one_wave below); otherwise ~8 waves of bands >= 256
+// rows in row-major order.
 static bool tile_masked(const sor_grid* g, int T, int s0, int strip, int64_t R0, int64_t R1) {
   const int64_t sw = s0 + (int64_t)strip * (kWaveCols - 4 * T);
   const int64_t i_first = (R0 - (2 * T - 1)) & ~1LL;
@@ -492,12 +491,15 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm
     *out = it->second;
     return SOR_OK;
   }
-  static double alpha = -1.0, waves = -1.0;
+  static double alpha = -1.0, alpha2 = -1.0, waves = -1.0;
   static int64_t min_h = 0;
   if (alpha < 0) {
     const char* e = getenv("SOR_WAVE_ALPHA");
-    alpha = e ? atof(e) : 1.7;
-    if (!(alpha >= 1.0)) alpha = 1.7;
+    alpha = e ? atof(e) : 1.33;  // edge-strip batch (SASS: 555/416 instructions at T=4)
+    if (!(alpha >= 1.0)) alpha = 1.33;
+    e = getenv("SOR_WAVE_ALPHA2");
+    alpha2 = e ? atof(e) : 1.3;  // row-masked batch (measured best on C3; SASS 647/416)
+    if (!(alpha2 >= 1.0)) alpha2 = 1.3;
     e = getenv("SOR_WAVE_WAVES");
     waves = e ? atof(e) : 0.0;  // 0 = automatic
     e = getenv("SOR_WAVE_MIN_BAND");
@@ -521,35 +523,66 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm
       r += h;
     }
   };
-  auto count = [&](double cost) {
-    std::vector<int4> tl;
-    for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
-    return (int64_t)tl.size();
+  std::vector<int4> tl;
+  // One-wave mode (every tile resident at once, so the launch lasts as long as
+  // its slowest tile).  A tile runs whole 6-step batches; its cost in
+  // unmasked-batch units mirrors the kernel's masking levels (run() in
+  // sor_kernels.cuh): batches updating a ring/padding row cost alpha2, the
+  // others alpha1 on an edge strip (column selects) and 1 elsewhere.  Each
+  // tile gets the most batches whose cost fits the budget Bc; Bc is the
+  // smallest budget whose tiles fit in one wave.
+  const int S = 2 * T;
+  auto tile_cost = [&](int w, int64_t R0, int64_t nb) -> double {
+    const int64_t sw = s0 + (int64_t)w * wout;
+    const bool col = !(sw >= 1 && sw + kWaveCols - 1 <= g->cols);
+    const int64_t i_first = (R0 - (S - 1)) & ~1LL;
+    const int64_t jA = std::min<int64_t>(nb, std::max<int64_t>(0, -floordiv6((int)(i_first - S))));
+    const int64_t jB = std::max<int64_t>(jA, std::min<int64_t>(nb, floordiv6((int)(g->rows - 5 - i_first)) + 1));
+    return (double)(jA + (nb - jB)) * alpha2 + (double)(jB - jA) * (col ? alpha : 1.0);
   };
-  double cost;
-  if (waves > 0) {
-    const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / nstrips);
-    cost = (double)std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb) + warm;
-  } else {
-    // smallest cost (shortest bands) that still fits one wave
-    double lo = 8 + warm, hi = (double)nrows + warm + 1;
-    if (count(hi) > slots) {
-      lo = hi;  // even whole-strip bands exceed a wave: many waves
-    } else {
-      for (int iter = 0; iter < 40; ++iter) {
-        const double mid = 0.5 * (lo + hi);
-        if (count(mid) <= slots) hi = mid; else lo = mid;
+  auto one_wave = [&](double Bc, std::vector<int4>* out_tl) -> int64_t {
+    int64_t n = 0;
+    for (int w = 0; w < nstrips; ++w) {
+      int64_t r = s.g_lo;
+      while (r < s.g_hi) {
+        const int64_t i_first = (r - (S - 1)) & ~1LL;
+        // batches needed to finish every remaining row of the strip
+        const int64_t nb_all = (s.g_hi + S - 1 - i_first + 5) / 6;
+        int64_t nb = std::min<int64_t>(nb_all, (int64_t)Bc);
+        while (nb > 1 && tile_cost(w, r, nb) > Bc) --nb;
+        const int64_t h = std::max<int64_t>(1, std::min(s.g_hi - r, i_first + 6 * nb - (S - 1) - r));
+        if (out_tl) out_tl->push_back(make_int4(w, (int)r, (int)(r + h), 0));
+        ++n;
+        r += h;
       }
     }
-    cost = hi;
-    const int64_t kOneWaveMaxH = 512, kMinH = min_h > 0 ? min_h : 256;
-    if (cost - warm > kOneWaveMaxH) {
+    return n;
+  };
+  double Bc = 0.0;
+  if (waves <= 0) {
+    const double kOneWaveMaxB = (512.0 + warm + 5) / 6;
+    for (double b = (double)((4 * T - 2 + 6) / 6 + 1); b <= kOneWaveMaxB; b += 0.125)
+      if (one_wave(b, nullptr) <= slots) {
+        Bc = b;
+        break;
+      }
+  }
+  if (Bc > 0) {
+    one_wave(Bc, &tl);
+  } else {
+    // many waves (C4, C5): ~8 waves of bands >= 256 rows; the block scheduler
+    // balances the load dynamically
+    double cost;
+    if (waves > 0) {
+      const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / nstrips);
+      cost = (double)std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb) + warm;
+    } else {
+      const int64_t kMinH = min_h > 0 ? min_h : 256;
       const int64_t nb8 = std::max<int64_t>(1, 8 * slots / nstrips);
       cost = (double)std::max<int64_t>(kMinH, (nrows + nb8 - 1) / nb8) + warm;
     }
+    for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
   }
-  std::vector<int4> tl;
-  for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
   // row-major order: warps running together stream neighbouring strips of the
   // same rows (shared ghost columns hit in L2, DRAM pages stay open)
   std::stable_sort(tl.begin(), tl.end(),

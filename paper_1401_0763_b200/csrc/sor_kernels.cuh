@@ -75,6 +75,8 @@ struct IterCtl {
   unsigned int nparts;  // number of ticket takers (warps or CTAs) in this launch
 };
 
+__host__ __device__ __forceinline__ int floordiv6(int x) { return x >= 0 ? x / 6 : -((5 - x) / 6); }
+
 // ---------------------------------------------------------------- arithmetic
 __device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
@@ -247,7 +249,7 @@ struct WaveArgs {
   long long g0;      // global row of storage row 0
   long long rows, cols;
   long long r_lo, r_hi;  // owned global rows written by this launch
-  const int4* tiles;  // per warp: (strip, R0, R1, masked) — see launch_wave_T
+  const int4* tiles;  // per tile: (strip, R0, R1, unused) — see wave_tiles
   int ntiles;
   int s0;            // first column of strip 0 (multiple of 4)
   R w;
@@ -377,6 +379,16 @@ __device__ __forceinline__ void stg4_if(bool p, float* a, const float (&x)[4]) {
                "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "r"((int)p)
                : "memory");
 }
+__device__ __forceinline__ void stg2_if(bool p, double* a, double x, double y) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.global.v2.f64 [%0], {%1,%2};\n}" ::"l"(a), "d"(x),
+               "d"(y), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ void stg2_if(bool p, float* a, float x, float y) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.global.v2.f32 [%0], {%1,%2};\n}" ::"l"(a), "f"(x),
+               "f"(y), "r"((int)p)
+               : "memory");
+}
 __device__ __forceinline__ void stg1_if(bool p, double* a, double x) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(a), "d"(x),
                "r"((int)p)
@@ -412,11 +424,14 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 //
 // CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each,
 // 3 = high 32 bits of |delta| of each (VIMNMX3, ~1.5 ALU ops per cell).
-// MASK: false for warps whose rows and columns are all interior cells (no
-// Dirichlet/padding cell to keep fixed).  Ownership (which computed cells
-// are valid and written: the strip minus its 2T ghost columns on each side,
-// the band's rows) applies to every warp.
-template <typename R, int T, int NST, int CK, bool MASK, int SB, int SE>
+// Masking (cells that must keep their value: the Dirichlet ring and the
+// padding around it) is chosen per 6-step batch, warp-uniformly: MK = 0 when
+// every cell the batch updates is interior, 1 when only columns of an edge
+// strip need it (a lane-constant select), 2 when the batch also updates a ring
+// or padding row (first/last batches of the top/bottom bands).  Ownership
+// (which computed cells are valid and written: the strip minus its 2T ghost
+// columns on each side, the band's rows) applies to every warp.
+template <typename R, int T, int NST, int CK, int SB, int SE>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
   static constexpr int NSLOT = CK >= 2 ? T : 1;
@@ -428,9 +443,12 @@ struct WavePipe {
   unsigned long long dmax[CK == 1 || CK == 2 ? NSLOT : 1];  // CK 1, 2: ordered bits
   unsigned int hmax[CK >= 3 ? NSLOT : 1];                     // CK 3, 4: high words
   unsigned int ownA, ownB;         // CK 3/4: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
-  bool upd[4], own[4];
-  bool own_all;
+  unsigned int pf[2];              // CK 4: all-ones iff this batch's probe row 0 / 1 is owned
+  bool upd[4];
+  bool ownP[2];                    // column pair (q0,q1) / (q2,q3) owned by position (see wave_tile)
   int rows, R0, R1;
+  int col_mask;                    // 1: edge strip (ring/padding columns), else 0
+  R* orow;                         // back: dst address of the row stage S-1 finishes at this step
   // ring: row n >= 2 in batch j = (n-2)/6, slot (j&1)*6 + (n-2)%6, barrier
   // j&1 (phase (j>>1)&1); rows n = 0,1 (prologue) first use slots 10, 11
   const R* ring;
@@ -459,7 +477,7 @@ struct WavePipe {
     bulk_g2s(ring_s + 11 * ROWB, gsrc + pitch, ROWB, bar);
   }
 
-  template <int M6>
+  template <int MK, int M6>
   __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, R* hp, long long c0) {
     constexpr int O = M6 & 1;
     constexpr int PH = M6 % 3;          // slot of age 0 (this step)
@@ -476,9 +494,9 @@ struct WavePipe {
       C[SB - 2][PH][0] = x[2];
       C[SB - 2][PH][1] = x[3];
     }
-    // CK 3/4: bit s set iff stage s's row i-s is owned (R0 <= i-s < R1)
+    // CK 3: bit s set iff stage s's row i-s is owned (R0 <= i-s < R1)
     unsigned int rowm = 0u;
-    if (CK >= 3) {
+    if (CK == 3) {
       const int lo_s = max(0, i - R1 + 1), hi_s = min(S - 1, i - R0);
       rowm = hi_s >= lo_s ? (((2u << hi_s) - 1u) & ~((1u << lo_s) - 1u)) : 0u;
     }
@@ -511,23 +529,33 @@ struct WavePipe {
       const R weB = (O == 0) ? mid : radd(w1, nb);
       R v0 = sor_update(radd(n0, s0), weA, u0, a.w);
       R v1 = sor_update(radd(n1, s1), weB, u1, a.w);
-      if (MASK) {
+      if (MK == 1) {
+        v0 = upd[O] ? v0 : u0;
+        v1 = upd[O + 2] ? v1 : u1;
+      } else if (MK == 2) {
         const bool rowok = (unsigned)(r - 1) < (unsigned)rows;
         v0 = (rowok && upd[O]) ? v0 : u0;
         v1 = (rowok && upd[O + 2]) ? v1 : u1;
       }
-      if (CK == 3 || (CK == 4 && probe_row(M6, s))) {
+      if (CK == 4 && probe_row(M6, s)) {
+        // probe rows of this batch: row i_first+6j (M6 == s) or 6 rows above
+        // (M6 == s-6); their ownership masks are set once per batch
+        const int pi = M6 < s ? 1 : 0;
+        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & ownA & pf[pi];
+        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & ownB & pf[pi];
+        hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
+      } else if (CK == 3) {
         // all-ones iff this stage's row is an owned row (bit s of rowm)
         const unsigned int fill = (unsigned int)((int)(rowm << (31 - s)) >> 31);
         const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & ownA & fill;
         const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & ownB & fill;
         hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
       } else if (CK != 0 && (CK == 2 || s >= S - 2)) {
-        const bool inb = (r >= R0) & (r < R1);
+        const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
         const int slot = CK == 2 ? (s >> 1) : 0;
         const unsigned long long d0 = delta_bits(v0, u0), d1 = delta_bits(v1, u1);
-        dmax[slot] = umax64(dmax[slot], (inb && own[O]) ? d0 : 0ull);
-        dmax[slot] = umax64(dmax[slot], (inb && own[O + 2]) ? d1 : 0ull);
+        dmax[slot] = umax64(dmax[slot], (inb && ownP[0]) ? d0 : 0ull);
+        dmax[slot] = umax64(dmax[slot], (inb && ownP[1]) ? d1 : 0ull);
       }
       if (s < S - 1) {
         C[s][PH][0] = v0;
@@ -535,18 +563,19 @@ struct WavePipe {
       } else {
         // finished row r: this stage's colour at q = O, O+2; the other colour
         // from stage S-2's row r (one step old, at q = 1-O, 3-O)
-        const bool inb = (r >= R0) & (r < R1);
+        const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
         R out[4];
         out[O] = v0;
         out[O + 2] = v1;
         out[1 - O] = C[S - 2][P1][0];
         out[3 - O] = C[S - 2][P1][1];
-        R* p = a.dst + (long long)(r - a.g0) * a.pitch + c0;
-        stg4_if(inb && own_all, p, out);
-        if (!own_all) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) stg1_if(inb && own[q], p + q, out[q]);
+        if (T % 2 == 0) {  // ghost bands are whole lanes
+          stg4_if(inb && ownP[0], orow, out);
+        } else {
+          stg2_if(inb && ownP[0], orow, out[0], out[1]);
+          stg2_if(inb && ownP[1], orow + 2, out[2], out[3]);
         }
+        orow += pitch;
       }
     }
     if (SE < S) {
@@ -561,16 +590,31 @@ struct WavePipe {
     }
   }
 
-  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, long long c0) {
-    constexpr bool front = SB == 0, back = SE == S;
-    constexpr bool split = !(front && back);
-    if (split && !front) {  // back warp: both handoff buffers start empty
-      named_bar_arrive(bar_empty + 0, 64);
-      if (nbatch > 1) named_bar_arrive(bar_empty + 1, 64);
-    }
+  template <int MK>
+  __device__ __forceinline__ void batch(const WaveArgs<R>& a, int i, const R* rowp, R* hp, long long c0) {
+    step<MK, 0>(a, i, rowp, hp, c0);
+    step<MK, 1>(a, i + 1, rowp, hp, c0);
+    step<MK, 2>(a, i + 2, rowp, hp, c0);
+    step<MK, 3>(a, i + 3, rowp, hp, c0);
+    step<MK, 4>(a, i + 4, rowp, hp, c0);
+    step<MK, 5>(a, i + 5, rowp, hp, c0);
+  }
+
+  // Batches [j0, j1) with masking level MK (one loop per level, so each loop
+  // keeps its own register assignment and no value is moved between levels).
+  template <int MK>
+  __device__ __forceinline__ void run_range(const WaveArgs<R>& a, int i_first, long long c0, int j0, int j1) {
+    constexpr bool front = SB == 0;
+    constexpr bool split = !(front && SE == S);
 #pragma unroll 1
-    for (int j = 0; j < nbatch; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const int m = 6 * j;
+      if (CK == 4) {
+        // probe rows of batch j: i_first+6j (stages s = M6) and i_first+6j-6 (s = M6+6)
+        const int rp = i_first + m;
+        pf[0] = (unsigned)(rp - R0) < (unsigned)(R1 - R0) ? 0xffffffffu : 0u;
+        pf[1] = (unsigned)(rp - 6 - R0) < (unsigned)(R1 - R0) ? 0xffffffffu : 0u;
+      }
       const R* rowp = nullptr;
       R* hp = split ? hand + (j & 1) * (6 * 32 * 4) : nullptr;
       if (front) {
@@ -580,12 +624,7 @@ struct WavePipe {
       } else {
         named_bar_sync(bar_full + (j & 1), 64);
       }
-      step<0>(a, i_first + m, rowp, hp, c0);
-      step<1>(a, i_first + m + 1, rowp, hp, c0);
-      step<2>(a, i_first + m + 2, rowp, hp, c0);
-      step<3>(a, i_first + m + 3, rowp, hp, c0);
-      step<4>(a, i_first + m + 4, rowp, hp, c0);
-      step<5>(a, i_first + m + 5, rowp, hp, c0);
+      batch<MK>(a, i_first + m, rowp, hp, c0);
       if (front) {
         if (split) named_bar_arrive(bar_full + (j & 1), 64);
         __syncwarp();
@@ -598,14 +637,34 @@ struct WavePipe {
       }
     }
   }
+
+  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, long long c0) {
+    constexpr bool front = SB == 0, back = SE == S;
+    constexpr bool split = !(front && back);
+    if (split && !front) {  // back warp: both handoff buffers start empty
+      named_bar_arrive(bar_empty + 0, 64);
+      if (nbatch > 1) named_bar_arrive(bar_empty + 1, 64);
+    }
+    // Batch j updates rows i_first+6j-(S-1) .. i_first+6j+5; they are all in
+    // [1, rows] for jA <= j < jB, where only an edge strip's columns need
+    // masking.  The first and last batches of the top/bottom bands mask rows.
+    const int jA = min(nbatch, max(0, -floordiv6(i_first - S)));            // ceil((S - i_first) / 6)
+    const int jB = max(jA, min(nbatch, floordiv6(rows - 5 - i_first) + 1));
+    run_range<2>(a, i_first, c0, 0, jA);
+    if (col_mask)
+      run_range<1>(a, i_first, c0, jA, jB);
+    else
+      run_range<0>(a, i_first, c0, jA, jB);
+    run_range<2>(a, i_first, c0, jB, nbatch);
+  }
 };
 
 // One warp (or warp pair) = one (strip, band) tile; tiles never synchronise.
-template <typename R, int T, int NST, int CK, bool MASK, int SB, int SE>
+template <typename R, int T, int NST, int CK, int SB, int SE>
 __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* wbase, R* hand, int bar_id,
                                           int lane, int sw, int R0, int R1, int i_first, int nsteps,
                                           unsigned long long (&dm)[kMaxT]) {
-  WavePipe<R, T, NST, CK, MASK, SB, SE> P;
+  WavePipe<R, T, NST, CK, SB, SE> P;
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) {
     if (CK == 1 || CK == 2) P.dmax[t] = 0ull;
@@ -623,27 +682,30 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
   P.R0 = R0;
   P.R1 = R1;
   const long long c0 = (long long)sw + 4 * lane;
-  const int olo = max(sw + 2 * T, 1);
-  const int ohi = min(sw + kWaveCols - 2 * T, (int)a.cols + 1);
-  P.own_all = true;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int c = (int)c0 + q;
     P.upd[q] = (c >= 1) && (c <= (int)a.cols);
-    P.own[q] = (c >= olo) && (c < ohi);
-    P.own_all = P.own_all && P.own[q];
   }
-  // CK 3 excludes only the strip's ghost columns (invalid values); ring and
-  // padding cells are never updated, so their |delta| is 0 anyway.  Cell A is
-  // q = O in {0,1}, cell B is q = O+2 in {2,3}; the ghost bands are 2T wide
-  // and start at multiples of 4, so they cover whole pairs and A/B validity
-  // does not depend on O.
+  P.col_mask = (sw >= 1 && sw + kWaveCols - 1 <= (int)a.cols) ? 0 : 1;
+  // Ownership by position: the strip minus its 2T ghost columns per side.
+  // The ghost bands are 2T wide and start at multiples of 4, so they cover
+  // whole column pairs (whole lanes for even T); cell A (q = O) is in pair 0,
+  // cell B (q = O+2) in pair 1.  Owned-by-position columns of different strips
+  // are disjoint.  Ring and padding columns inside it are never updated: they
+  // carry their source value through every stage, so storing them rewrites
+  // the value they hold and their |delta| is 0.  Stores and maxima therefore
+  // need no per-column test against [1, cols].
   {
     const int g_lo = sw + 2 * T, g_hi = sw + kWaveCols - 2 * T;
     const int cA = (int)c0, cB = (int)c0 + 2;
-    P.ownA = (cA >= g_lo && cA + 1 < g_hi) ? 0x7fffffffu : 0u;
-    P.ownB = (cB >= g_lo && cB + 1 < g_hi) ? 0x7fffffffu : 0u;
+    P.ownP[0] = cA >= g_lo && cA + 1 < g_hi;
+    P.ownP[1] = cB >= g_lo && cB + 1 < g_hi;
+    P.ownA = P.ownP[0] ? 0x7fffffffu : 0u;
+    P.ownB = P.ownP[1] ? 0x7fffffffu : 0u;
   }
+  // row finished by stage S-1 at step 0 is i_first - (S-1)
+  P.orow = a.dst + (long long)(i_first - (2 * T - 1) - a.g0) * a.pitch + c0;
 #pragma unroll
   for (int s = 0; s < 2 * T - 1; ++s)
 #pragma unroll
@@ -712,34 +774,17 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
     // i_first even; nsteps a multiple of 6 (ring phase x parity)
     const int i_first = (R0 - (2 * T - 1)) & ~1;
     const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
-#ifdef SOR_EXPERIMENT_FORCE_UNMASKED  // timing experiments only: wrong results at the edges
-    const bool interior = true;
-#else
-    // the host's classification (tile.w) is re-derived here as a safety net
-    const bool interior = !tile.w && (sw >= 1) && (sw + kWaveCols - 1 <= (int)a.cols) &&
-                          (i_first - 1 >= 1) && (i_first + nsteps <= (int)a.rows);
-#endif
     if (SPLIT) {
       unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST>();
       R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST>());
       const int bar_id = 1 + 4 * slot;  // named barriers 1..8 (0 is __syncthreads)
-      if (role == 0) {
-        if (interior)
-          wave_tile<R, T, NST, CK, false, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
-        else
-          wave_tile<R, T, NST, CK, true, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
-      } else {
-        if (interior)
-          wave_tile<R, T, NST, CK, false, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
-        else
-          wave_tile<R, T, NST, CK, true, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
-      }
+      if (role == 0)
+        wave_tile<R, T, NST, CK, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+      else
+        wave_tile<R, T, NST, CK, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
     } else {
       unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
-      if (interior)
-        wave_tile<R, T, NST, CK, false, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
-      else
-        wave_tile<R, T, NST, CK, true, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+      wave_tile<R, T, NST, CK, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
     }
   }
   (void)role;
