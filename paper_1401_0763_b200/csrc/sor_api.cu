@@ -10,6 +10,8 @@
 // per half-sweep for K1, h = 2T per T-iteration pass for K3/K4) and, on
 // checked iterations, the per-slab max is joined by an allreduce-max.  The
 // transport is NCCL over NVLink (dist mode) or device copies (virtual mode).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -38,6 +40,7 @@ struct Slab {
   int64_t g0 = 0;              // global row of storage row 0 (= g_lo - kRowPad)
   int64_t nstore = 0;          // storage rows
   void* plane[2] = {nullptr, nullptr};
+  CUtensorMap tmap[2];  // 2-D tensor maps of the planes (wave kernel source rows)
 };
 
 enum class Mode { Single, Virtual, Dist };
@@ -146,6 +149,29 @@ cudaMemcpyKind kDefault = cudaMemcpyDefault;
 // ------------------------------------------------------------------ layout
 // Copy global rows [ga, gb) of a full (rows+2)x(cols+2) fp64 array into plane p
 // of slab s (rounding to fp32 if needed).
+// Tensor map of one storage plane for the wave kernel's TMA row loads: the
+// whole (nstore x pitch) plane, boxes of 6 rows x kWaveCols columns.
+int make_tmap(sor_grid* g, Slab& s, int p) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return set_error(g, SOR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)g->pitch, (cuuint64_t)s.nstore};
+  const cuuint64_t strides[1] = {(cuuint64_t)(g->pitch * g->esz)};
+  const cuuint32_t box[2] = {(cuuint32_t)kWaveCols, 6u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = encode(&s.tmap[p], g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      s.plane[p], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(g, SOR_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SOR_OK;
+}
+
 int load_rows(sor_grid* g, const Slab& s, int p, const double* init, int64_t ga, int64_t gb) {
   if (gb <= ga) return SOR_OK;
   const int64_t w = g->cols + 2;
@@ -295,6 +321,7 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
       }
     }
     g->slabs.push_back(s);
+    for (int p = 0; p < 2; ++p) TRY(make_tmap(g, g->slabs.back(), p));
   }
   const bool on_dev = is_device_ptr(init);
   TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
@@ -637,7 +664,7 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks;
-  wave_kernel<R, T, NST, CK, SPLIT><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c);
+  wave_kernel<R, T, NST, CK, SPLIT><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c, s.tmap[g->cur]);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
   return SOR_OK;

@@ -29,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sorb {
@@ -333,6 +334,15 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// 2-D tensor TMA: a box of 6 rows x kWaveCols columns (tensor map built by
+// the host over the whole storage plane, see make_tmap in sor_api.cu).
+__device__ __forceinline__ void tma_rows(uint32_t dst, const CUtensorMap* tm, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(tm), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -454,6 +464,8 @@ struct WavePipe {
   const R* ring;
   uint32_t ring_s, bar_s;
   const R* gsrc;              // global address of (row i_first-1, column s_w)
+  const CUtensorMap* tm;      // tensor map of the source plane; (tm_x, tm_y) = storage (column, row) of gsrc
+  int tm_x, tm_y;
   long long pitch;
   int nbatch;
   int lane;
@@ -463,6 +475,12 @@ struct WavePipe {
 
   // lane 0: rows k_lo..k_hi-1 of batch j (expect_tx covers the whole batch
   // when k_lo == 0; a second call completes it)
+  // lane 0, steady state: the 6 rows of batch j as one tensor-TMA box
+  __device__ __forceinline__ void issue_batch_tma(int j) {
+    const uint32_t bar = bar_s + 8u * (j & 1);
+    mbar_expect_tx(bar, 6 * ROWB);
+    tma_rows(ring_s + (j & 1) * 6 * ROWB, tm, tm_x, tm_y + 6 * j + 2, bar);
+  }
   __device__ __forceinline__ void issue_batch(int j, int k_lo = 0, int k_hi = 6) {
     const uint32_t bar = bar_s + 8u * (j & 1);
     if (k_lo == 0) mbar_expect_tx(bar, 6 * ROWB);
@@ -628,10 +646,9 @@ struct WavePipe {
       if (front) {
         if (split) named_bar_arrive(bar_full + (j & 1), 64);
         __syncwarp();
-        if (lane == 0 && j + 2 < nbatch) {
-          fence_proxy_async_smem();  // our generic reads of the slots precede the async refill
-          issue_batch(j + 2);
-        }
+        // every lane's reads of this half of the ring completed (their values
+        // were consumed in the batch) before lane 0 refills it
+        if (lane == 0 && j + 2 < nbatch) issue_batch_tma(j + 2);
       } else if (j + 2 < nbatch) {
         named_bar_arrive(bar_empty + (j & 1), 64);
       }
@@ -661,7 +678,7 @@ struct WavePipe {
 
 // One warp (or warp pair) = one (strip, band) tile; tiles never synchronise.
 template <typename R, int T, int NST, int CK, int SB, int SE>
-__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* wbase, R* hand, int bar_id,
+__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMap* tm, unsigned char* wbase, R* hand, int bar_id,
                                           int lane, int sw, int R0, int R1, int i_first, int nsteps,
                                           unsigned long long (&dm)[kMaxT]) {
   WavePipe<R, T, NST, CK, SB, SE> P;
@@ -712,6 +729,9 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, unsigned char* w
     for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
   P.pitch = a.pitch;
   P.gsrc = a.src + (long long)(i_first - 1 - a.g0) * a.pitch + sw;
+  P.tm = tm;
+  P.tm_x = kColPad + sw;
+  P.tm_y = i_first - 1 - (int)a.g0;
   P.nbatch = nsteps / 6;
   if (SB == 0) {
     if (lane == 0) {
@@ -756,7 +776,7 @@ __host__ __device__ constexpr int wave_smem_bytes() {
 
 template <typename R, int T, int NST, int CK, bool SPLIT>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
-    wave_kernel(WaveArgs<R> a, IterCtl ctl) {
+    wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ CUtensorMap tm) {
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
   extern __shared__ __align__(128) unsigned char wave_smem[];
   const int lane = threadIdx.x & 31;
@@ -779,12 +799,12 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
       R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST>());
       const int bar_id = 1 + 4 * slot;  // named barriers 1..8 (0 is __syncthreads)
       if (role == 0)
-        wave_tile<R, T, NST, CK, 0, T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, 0, T>(a, &tm, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
       else
-        wave_tile<R, T, NST, CK, T, 2 * T>(a, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, T, 2 * T>(a, &tm, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
     } else {
       unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
-      wave_tile<R, T, NST, CK, 0, 2 * T>(a, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+      wave_tile<R, T, NST, CK, 0, 2 * T>(a, &tm, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
     }
   }
   (void)role;
