@@ -40,7 +40,7 @@ struct Slab {
   int64_t g0 = 0;              // global row of storage row 0 (= g_lo - kRowPad)
   int64_t nstore = 0;          // storage rows
   void* plane[2] = {nullptr, nullptr};
-  CUtensorMap tmap[2];  // 2-D tensor maps of the planes (wave kernel source rows)
+  WaveMaps tmap[2];  // per plane: tensor maps of the wave kernel's source-row boxes
 };
 
 enum class Mode { Single, Virtual, Dist };
@@ -149,9 +149,10 @@ cudaMemcpyKind kDefault = cudaMemcpyDefault;
 // ------------------------------------------------------------------ layout
 // Copy global rows [ga, gb) of a full (rows+2)x(cols+2) fp64 array into plane p
 // of slab s (rounding to fp32 if needed).
-// Tensor map of one storage plane for the wave kernel's TMA row loads: the
-// whole (nstore x pitch) plane, boxes of 6 rows x kWaveCols columns.
-int make_tmap(sor_grid* g, Slab& s, int p) {
+// Tensor maps of one storage plane for the wave kernel's TMA row loads: the
+// whole (nstore x pitch) plane, boxes of 6 rows (steady state) and 2 rows
+// (prologue) x one warp strip (32 * kWaveNC columns).
+int make_tmaps(sor_grid* g, Slab& s, int p) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -163,12 +164,14 @@ int make_tmap(sor_grid* g, Slab& s, int p) {
   }
   const cuuint64_t dims[2] = {(cuuint64_t)g->pitch, (cuuint64_t)s.nstore};
   const cuuint64_t strides[1] = {(cuuint64_t)(g->pitch * g->esz)};
-  const cuuint32_t box[2] = {(cuuint32_t)kWaveCols, 6u};
   const cuuint32_t estr[2] = {1u, 1u};
-  CUresult r = encode(&s.tmap[p], g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                      s.plane[p], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(g, SOR_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  for (int b = 0; b < 2; ++b) {
+    const cuuint32_t box[2] = {(cuuint32_t)wave_cols<kWaveNC>(), b == 0 ? 6u : 2u};
+    CUresult r = encode(&s.tmap[p].m[b], g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        2, s.plane[p], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(g, SOR_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
   return SOR_OK;
 }
 
@@ -289,7 +292,7 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
   g->nsm = prop.multiProcessorCount;
   g->esz = g->dt == SOR_F64 ? 8 : 4;
   // row: [kColPad][cols+2][>= one strip of read-ahead], multiple of 32 elements
-  g->pitch = round_up(kColPad + g->cols + 2 + kWaveCols + 16, 32);
+  g->pitch = round_up(kColPad + g->cols + 2 + wave_cols<kWaveNC>() + 16, 32);
   CU(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
   g->stream = g->own_stream;
   CU(cudaEventCreate(&g->ev0));
@@ -321,7 +324,7 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
       }
     }
     g->slabs.push_back(s);
-    for (int p = 0; p < 2; ++p) TRY(make_tmap(g, g->slabs.back(), p));
+    for (int p = 0; p < 2; ++p) TRY(make_tmaps(g, g->slabs.back(), p));
   }
   const bool on_dev = is_device_ptr(init);
   TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
@@ -492,7 +495,7 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
 
 // ------------------------------------------------------------------ K3/K4
 template <typename R>
-constexpr int wave_nst() { return 12; }
+constexpr int wave_nst() { return 14; }
 
 // ------------------------------------------------------------------ tiles
 // One warp (pair) per tile = (strip, band of owned rows).  A tile runs whole
@@ -502,17 +505,17 @@ constexpr int wave_nst() { return 12; }
 // resident tiles gives bands <= 512 rows the launch is exactly one wave with
 // batch counts equalised (one_wave below); otherwise ~8 waves of bands >= 256
 // rows in row-major order.
-static bool tile_masked(const sor_grid* g, int T, int s0, int strip, int64_t R0, int64_t R1) {
-  const int64_t sw = s0 + (int64_t)strip * (kWaveCols - 4 * T);
+static bool tile_masked(const sor_grid* g, int T, int wc, int s0, int strip, int64_t R0, int64_t R1) {
+  const int64_t sw = s0 + (int64_t)strip * (wc - 4 * T);
   const int64_t i_first = (R0 - (2 * T - 1)) & ~1LL;
   const int64_t nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
-  return !((sw >= 1) && (sw + kWaveCols - 1 <= g->cols) && (i_first - 1 >= 1) &&
+  return !((sw >= 1) && (sw + wc - 1 <= g->cols) && (i_first - 1 >= 1) &&
            (i_first + nsteps <= g->rows));
 }
 
-int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm, bool split, int s0,
+int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tiles_per_sm, bool split, int s0,
                std::pair<int4*, int>* out) {
-  const auto key = std::make_tuple(slab_idx, T * 2 + (split ? 1 : 0), tiles_per_sm);
+  const auto key = std::make_tuple(slab_idx, (T * 2 + (split ? 1 : 0)) * 1024 + wc, tiles_per_sm);
   auto it = g->tiles.find(key);
   if (it != g->tiles.end()) {
     *out = it->second;
@@ -532,7 +535,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm
     e = getenv("SOR_WAVE_MIN_BAND");
     min_h = e ? atoll(e) : 0;
   }
-  const int64_t wout = kWaveCols - 4 * T;
+  const int64_t wout = wc - 4 * T;
   const int nstrips = (int)((g->cols + 1 - (s0 + 2 * T) + wout - 1) / wout);
   const int64_t nrows = s.g_hi - s.g_lo;
   const int64_t slots = (int64_t)g->nsm * tiles_per_sm;
@@ -543,10 +546,10 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm
     while (r < s.g_hi) {
       // try an unmasked-height band first; fall back to the masked height
       int64_t h = std::max<int64_t>(8, (int64_t)(cost - warm));
-      bool m = tile_masked(g, T, s0, w, r, std::min(r + h, s.g_hi));
+      bool m = tile_masked(g, T, wc, s0, w, r, std::min(r + h, s.g_hi));
       if (m) h = std::max<int64_t>(8, (int64_t)(cost / alpha - warm));
       h = std::min<int64_t>(h, s.g_hi - r);
-      if (tl) tl->push_back(make_int4(w, (int)r, (int)(r + h), tile_masked(g, T, s0, w, r, r + h) ? 1 : 0));
+      if (tl) tl->push_back(make_int4(w, (int)r, (int)(r + h), tile_masked(g, T, wc, s0, w, r, r + h) ? 1 : 0));
       r += h;
     }
   };
@@ -561,7 +564,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int tiles_per_sm
   const int S = 2 * T;
   auto tile_cost = [&](int w, int64_t R0, int64_t nb) -> double {
     const int64_t sw = s0 + (int64_t)w * wout;
-    const bool col = !(sw >= 1 && sw + kWaveCols - 1 <= g->cols);
+    const bool col = !(sw >= 1 && sw + wc - 1 <= g->cols);
     const int64_t i_first = (R0 - (S - 1)) & ~1LL;
     const int64_t jA = std::min<int64_t>(nb, std::max<int64_t>(0, -floordiv6((int)(i_first - S))));
     const int64_t jB = std::max<int64_t>(jA, std::min<int64_t>(nb, floordiv6((int)(g->rows - 5 - i_first)) + 1));
@@ -633,15 +636,15 @@ bool wave_split(int T) {
   return sp != 0 && T >= 2;
 }
 
-template <typename R, int T, int CK, bool SPLIT>
+template <typename R, int T, int CK, bool SPLIT, int NC>
 int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   constexpr int NST = wave_nst<R>();
-  constexpr int smem = wave_smem_bytes<R, NST, SPLIT>();
+  constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
   constexpr int per_cta = wave_tiles_per_cta(SPLIT);
   static int occ = 0;  // resident CTAs/SM for this instance
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT>, kWaveWarps * 32, smem);
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT, NC>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -657,14 +660,14 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   a.s0 = -4 * ((2 * T + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, T, occ * per_cta, SPLIT, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
   a.tiles = tt.first;
   a.ntiles = tt.second;
   const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta);
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks;
-  wave_kernel<R, T, NST, CK, SPLIT><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c, s.tmap[g->cur]);
+  wave_kernel<R, T, NST, CK, SPLIT, NC><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c, s.tmap[g->cur]);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
   return SOR_OK;
@@ -672,8 +675,10 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
 
 template <typename R, int T, int CK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
-  if (T >= 2 && wave_split(T)) return launch_wave_TS<R, T, CK, (T >= 2)>(g, s, w, ctl, fused_fin);
-  return launch_wave_TS<R, T, CK, false>(g, s, w, ctl, fused_fin);
+  // 4 columns per lane: wider lanes (NC = 6, 8; bitwise equal) measured
+  // slower on B200 at every T (fewer resident warps outweigh the extra ILP)
+  if (T >= 2 && wave_split(T)) return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
+  return launch_wave_TS<R, T, CK, false, kWaveNC>(g, s, w, ctl, fused_fin);
 }
 
 template <typename R, int CK>
@@ -974,7 +979,17 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         // near convergence (exact max within 16x tol) probing would keep
         // failing: switch to all cells.  Far from it (e.g. a probe that saw
         // only still-unchanged rows) keep probing.
-        if (ex.max_change < 16.0 * tol) g->every_ck = 3;
+        {
+          static double sw = -1.0;
+          if (sw < 0) {
+            const char* e = getenv("SOR_SOLVE_SWITCH");
+            sw = e ? atof(e) : 16.0;
+          }
+          if (getenv("SOR_DEBUG"))
+            fprintf(stderr, "[sor] re-run at %lld: probe hi %.6e exact %.6e (tol %.3e)\n", (long long)hs.amb_iter,
+                    hs.max_change, ex.max_change, tol);
+          if (ex.max_change < sw * tol) g->every_ck = 3;
+        }
         k = k_end + 1;  // g->cur now holds X_{k_end}
         if (k > maxit) {
           done = maxit;

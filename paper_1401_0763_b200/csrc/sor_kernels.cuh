@@ -37,7 +37,7 @@ namespace sorb {
 constexpr int kColPad = 32;   // storage columns left of global column 0
 constexpr int kRowPad = 24;   // storage rows above/below a slab's owned rows + halo
 constexpr int kWaveWarps = 4; // warps per CTA in wave_kernel (independent warps)
-constexpr int kWaveCols = 128;  // columns per warp strip (4 per lane)
+constexpr int kWaveNC = 4;     // columns per lane in wave_kernel (strip = 32*kWaveNC columns)
 
 constexpr int kMaxT = 4;      // max temporal depth (iterations per HBM pass)
 
@@ -94,6 +94,16 @@ __device__ __forceinline__ R sor_update(R ns, R we, R u, R w) {
   const R a = rmul(R(0.25), s);
   const R r = rsub(a, u);
   return radd(u, rmul(w, r));
+}
+
+// Same, also returning the correction p = w*r (u' = u + p).
+template <typename R>
+__device__ __forceinline__ R sor_update_p(R ns, R we, R u, R w, R& p) {
+  const R s = radd(ns, we);
+  const R a = rmul(R(0.25), s);
+  const R r = rsub(a, u);
+  p = rmul(w, r);
+  return radd(u, p);
 }
 
 // |u' - u| as ordered u64 bits; fp32 widened exactly first.
@@ -242,6 +252,12 @@ __global__ void __launch_bounds__(256) k1_half_sweep(R* base, long long pitch, l
 }
 
 // ---------------------------------------------------------------- K3 / K4
+// The two tensor maps of a source plane (6-row and 2-row boxes), passed by
+// value as one __grid_constant__ kernel parameter.
+struct WaveMaps {
+  CUtensorMap m[2];
+};
+
 template <typename R>
 struct WaveArgs {
   const R* src;      // column 0 of storage row 0 (plane + kColPad)
@@ -334,8 +350,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
-// 2-D tensor TMA: a box of 6 rows x kWaveCols columns (tensor map built by
-// the host over the whole storage plane, see make_tmap in sor_api.cu).
+// 2-D tensor TMA of a box of rows x one warp strip (tensor maps built by the
+// host over the whole storage plane, see make_tmaps in sor_api.cu); x, y =
+// storage column and row of the box corner.  (A 4-D view that interleaves
+// lanes' 16-B chunks in shared memory avoids the 2-way bank conflicts of the
+// row-major box but measured 25% slower end to end: 16-B inner boxes are slow
+// to fetch.)
 __device__ __forceinline__ void tma_rows(uint32_t dst, const CUtensorMap* tm, int x, int y, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -346,47 +366,85 @@ __device__ __forceinline__ void tma_rows(uint32_t dst, const CUtensorMap* tm, in
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void lds4(const double* p, double (&x)[4]) {
-  const double2 a = reinterpret_cast<const double2*>(p)[0];
-  const double2 b = reinterpret_cast<const double2*>(p)[1];
-  x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+// Generic shared-memory vector moves of N values (N even), 16-B aligned.
+template <int N>
+__device__ __forceinline__ void ldsN(const double* p, double (&x)[N]) {
+#pragma unroll
+  for (int k = 0; k < N / 2; ++k) {
+    const double2 v = reinterpret_cast<const double2*>(p)[k];
+    x[2 * k] = v.x;
+    x[2 * k + 1] = v.y;
+  }
 }
-__device__ __forceinline__ void lds4(const float* p, float (&x)[4]) {
-  const float4 a = *reinterpret_cast<const float4*>(p);
-  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+template <int N>
+__device__ __forceinline__ void ldsN(const float* p, float (&x)[N]) {
+  if (N % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < N / 4; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(p)[k];
+      x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      const float2 v = reinterpret_cast<const float2*>(p)[k];
+      x[2 * k] = v.x;
+      x[2 * k + 1] = v.y;
+    }
+  }
+}
+template <int N>
+__device__ __forceinline__ void stsN(double* p, const double (&x)[N]) {
+#pragma unroll
+  for (int k = 0; k < N / 2; ++k) reinterpret_cast<double2*>(p)[k] = make_double2(x[2 * k], x[2 * k + 1]);
+}
+template <int N>
+__device__ __forceinline__ void stsN(float* p, const float (&x)[N]) {
+  if (N % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < N / 4; ++k)
+      reinterpret_cast<float4*>(p)[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) reinterpret_cast<float2*>(p)[k] = make_float2(x[2 * k], x[2 * k + 1]);
+  }
 }
 
-// Shared memory of wave_kernel per warp: 2 batches of 6 source rows (12 slots
-// of kWaveCols values; the 2 prologue rows borrow the last two slots of batch
-// 1 until they are read), then 3 mbarriers (one per batch, one for the
-// prologue).  NST is the number of row slots (12).
-template <typename R, int NST>
+// Wave-kernel geometry.  NC columns per lane (4, 6 or 8), so a warp strip is
+// 32*NC columns; a lane holds NH = NC/2 cells of each colour per row.
+template <int NC>
+__host__ __device__ constexpr int wave_cols() { return 32 * NC; }
+
+// Shared memory of one tile's source ring: 2 batches of 6 source rows and the
+// 2 prologue rows (NST = 14 slots of 32*NC values, row-major), then 3
+// mbarriers (one per batch, one for the prologue).
+template <typename R, int NST, int NC>
 __host__ __device__ constexpr int wave_smem_per_warp() {
-  return (NST * kWaveCols * (int)sizeof(R) + 3 * 8 + 127) / 128 * 128;  // 128-B aligned bases
+  return (NST * wave_cols<NC>() * (int)sizeof(R) + 3 * 8 + 127) / 128 * 128;  // 128-B aligned bases
 }
 // Split mode: a warp PAIR shares one tile.  The front warp streams the source
 // and runs stages [0, T), the back warp runs stages [T, 2T); per step the
-// front hands over its last two stages' outputs (4 values per lane) through a
-// 2-batch shared ring synchronised with named barriers.  Half the registers
-// per warp -> twice the resident warps, and no spills at T = 4.
-template <typename R>
+// front hands over stage T-1's new row and stage T-2's row of two steps ago
+// (NC values per lane) through a 2-batch shared ring synchronised with named
+// barriers.  Half the registers per warp -> twice the resident warps.
+template <typename R, int NC>
 __host__ __device__ constexpr int wave_handoff_bytes() {
-  return 2 * 6 * 32 * 4 * (int)sizeof(R);  // 2 batches x 6 steps x 32 lanes x 4 values
+  return 2 * 6 * 32 * NC * (int)sizeof(R);  // 2 batches x 6 steps x 32 lanes x NC values
 }
-template <typename R, int NST>
+template <typename R, int NST, int NC>
 __host__ __device__ constexpr int wave_smem_per_pair() {
-  return wave_smem_per_warp<R, NST>() + wave_handoff_bytes<R>();
+  return wave_smem_per_warp<R, NST, NC>() + wave_handoff_bytes<R, NC>();
 }
 
 // Predicated stores (branch-free, so unrolled steps form one basic block).
-__device__ __forceinline__ void stg4_if(bool p, double* a, const double (&x)[4]) {
+__device__ __forceinline__ void stg4_if(bool p, double* a, double x0, double x1, double x2, double x3) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f64 [%0], {%1,%2,%3,%4};\n}" ::"l"(a),
-               "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3]), "r"((int)p)
+               "d"(x0), "d"(x1), "d"(x2), "d"(x3), "r"((int)p)
                : "memory");
 }
-__device__ __forceinline__ void stg4_if(bool p, float* a, const float (&x)[4]) {
+__device__ __forceinline__ void stg4_if(bool p, float* a, float x0, float x1, float x2, float x3) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f32 [%0], {%1,%2,%3,%4};\n}" ::"l"(a),
-               "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "r"((int)p)
+               "f"(x0), "f"(x1), "f"(x2), "f"(x3), "r"((int)p)
                : "memory");
 }
 __device__ __forceinline__ void stg2_if(bool p, double* a, double x, double y) {
@@ -399,16 +457,6 @@ __device__ __forceinline__ void stg2_if(bool p, float* a, float x, float y) {
                "f"(y), "r"((int)p)
                : "memory");
 }
-__device__ __forceinline__ void stg1_if(bool p, double* a, double x) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(a), "d"(x),
-               "r"((int)p)
-               : "memory");
-}
-__device__ __forceinline__ void stg1_if(bool p, float* a, float x) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(a), "f"(x),
-               "r"((int)p)
-               : "memory");
-}
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -418,22 +466,23 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 
 // Register pipeline of one warp.
 //
-// Lane columns c0..c0+3 (q = 0..3), c0 = s_w + 4*lane.  Step m has front row
-// i = i_first + m; it consumes source row i+1 and stage s (half-sweep s of the
-// pass, colour s&1) updates row i-s.  With O = i & 1 (= m & 1), the cells of
-// stage s in row i-s sit at q = O and O+2; a stage keeps only its own colour
-// ("compact pair" v[0] <-> q=O, v[1] <-> q=O+2 of the step that made it).
-// Rows are held in 3-slot rings indexed by (step mod 3), so with the loop
-// unrolled 6 ways (parity x ring phase) every register index is static and
-// no value is ever moved.  Source rows arrive through an NST-deep shared
-// ring filled by TMA bulk copies issued NST rows ahead.
+// Lane columns c0..c0+NC-1 (q = 0..NC-1), c0 = s_w + NC*lane.  Step m has
+// front row i = i_first + m; it consumes source row i+1 and stage s
+// (half-sweep s of the pass, colour s&1) updates row i-s.  With O = i & 1
+// (= m & 1), the cells of stage s in row i-s sit at q = O + 2h, h < NH; a
+// stage keeps only its own colour ("compact" v[h] <-> q = O+2h of the step
+// that made it).  Rows are held in 3-slot rings indexed by (step mod 3), so
+// with the loop unrolled 6 ways (parity x ring phase) every register index is
+// static and no value is ever moved.  Source rows arrive through an NST-deep
+// shared ring filled by TMA, 6 rows per box.
 //
 // This warp runs stages [SB, SE) of the S = 2T stages: SB == 0 streams the
-// source; SB > 0 receives stages SB-1, SB-2 from the front warp; SE < S hands
-// stages SE-1, SE-2 on; SE == S writes finished rows.
+// source; SB > 0 receives stage SB-1's new row and stage SB-2's row of two
+// steps ago from the front warp; SE < S hands the same on; SE == S writes
+// finished rows.
 //
 // CK: 0 = no max-change, 1 = of the pass's last iteration, 2 = of each,
-// 3 = high 32 bits of |delta| of each (VIMNMX3, ~1.5 ALU ops per cell).
+// 3 = high 32 bits of |delta| of each (VIMNMX3), 4 = as 3 on probe rows.
 // Masking (cells that must keep their value: the Dirichlet ring and the
 // padding around it) is chosen per 6-step batch, warp-uniformly: MK = 0 when
 // every cell the batch updates is interior, 1 when only columns of an edge
@@ -441,21 +490,25 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 // or padding row (first/last batches of the top/bottom bands).  Ownership
 // (which computed cells are valid and written: the strip minus its 2T ghost
 // columns on each side, the band's rows) applies to every warp.
-template <typename R, int T, int NST, int CK, int SB, int SE>
+template <typename R, int T, int NST, int CK, int SB, int SE, int NC>
 struct WavePipe {
   static constexpr int S = 2 * T;  // stages (half-sweeps) per pass
+  static constexpr int NH = NC / 2;
+  static constexpr int WC = wave_cols<NC>();
   static constexpr int NSLOT = CK >= 2 ? T : 1;
+  // ghost bands (2T columns) cover whole lanes: one ownership flag per lane
+  static constexpr bool LANE_OWN = (2 * T) % NC == 0;
   // CK 4 probes the rows with (row - i_first) % 6 == 0: in the 6-step
   // unrolled loop that is the compile-time condition (M6 - s) % 6 == 0
   __host__ __device__ static constexpr bool probe_row(int M6, int s) { return ((M6 - s) % 6 + 6) % 6 == 0; }
-  R F[3][4];                  // source rows, slot = (row - (i_first-1)) % 3 (front warp)
-  R C[S - 1][3][2];           // stage outputs, slot = step % 3 (unused stages vanish)
+  R F[3][NC];                 // source rows, slot = (row - (i_first-1)) % 3 (front warp)
+  R C[S - 1][3][NH];          // stage outputs, slot = step % 3 (unused stages vanish)
   unsigned long long dmax[CK == 1 || CK == 2 ? NSLOT : 1];  // CK 1, 2: ordered bits
   unsigned int hmax[CK >= 3 ? NSLOT : 1];                     // CK 3, 4: high words
-  unsigned int ownA, ownB;         // CK 3/4: 0x7fffffff if cell q=O (A) / q=O+2 (B) is owned
+  unsigned int ownM[NH];           // CK 3/4: 0x7fffffff if column pair h is owned
   unsigned int pf[2];              // CK 4: all-ones iff this batch's probe row 0 / 1 is owned
-  bool upd[4];
-  bool ownP[2];                    // column pair (q0,q1) / (q2,q3) owned by position (see wave_tile)
+  bool upd[NC];
+  bool ownP[NH];                   // column pair (q=2h, 2h+1) owned by position (see wave_tile)
   int rows, R0, R1;
   int col_mask;                    // 1: edge strip (ring/padding columns), else 0
   R* orow;                         // back: dst address of the row stage S-1 finishes at this step
@@ -463,54 +516,78 @@ struct WavePipe {
   // j&1 (phase (j>>1)&1); rows n = 0,1 (prologue) first use slots 10, 11
   const R* ring;
   uint32_t ring_s, bar_s;
-  const R* gsrc;              // global address of (row i_first-1, column s_w)
-  const CUtensorMap* tm;      // tensor map of the source plane; (tm_x, tm_y) = storage (column, row) of gsrc
+  const CUtensorMap* tm;      // tensor maps of the source plane (6-row and 2-row boxes);
+  const CUtensorMap* tm2;     // (tm_x, tm_y) = storage (column, row) of (i_first-1, s_w)
   int tm_x, tm_y;
   long long pitch;
   int nbatch;
   int lane;
-  R* hand;                    // split: handoff ring [2][6][32][4]
+  R* hand;                    // split: handoff ring [2][6][32][NC]
   int bar_full, bar_empty;    // split: named barrier ids (+ batch parity)
-  static constexpr uint32_t ROWB = kWaveCols * sizeof(R);
+  static constexpr uint32_t ROWB = WC * sizeof(R);
+  static constexpr int CH = 16 / (int)sizeof(R);  // values per 16-B chunk
 
-  // lane 0: rows k_lo..k_hi-1 of batch j (expect_tx covers the whole batch
-  // when k_lo == 0; a second call completes it)
-  // lane 0, steady state: the 6 rows of batch j as one tensor-TMA box
+  // lane 0: the 6 rows of batch j as one tensor-TMA box (rows 2+6j .. 7+6j
+  // counted from i_first-1)
   __device__ __forceinline__ void issue_batch_tma(int j) {
     const uint32_t bar = bar_s + 8u * (j & 1);
     mbar_expect_tx(bar, 6 * ROWB);
     tma_rows(ring_s + (j & 1) * 6 * ROWB, tm, tm_x, tm_y + 6 * j + 2, bar);
   }
-  __device__ __forceinline__ void issue_batch(int j, int k_lo = 0, int k_hi = 6) {
-    const uint32_t bar = bar_s + 8u * (j & 1);
-    if (k_lo == 0) mbar_expect_tx(bar, 6 * ROWB);
-#pragma unroll 1
-    for (int k = k_lo; k < k_hi; ++k)
-      bulk_g2s(ring_s + ((j & 1) * 6 + k) * ROWB, gsrc + (long long)(6 * j + 2 + k) * pitch, ROWB, bar);
-  }
-  __device__ __forceinline__ void issue_prologue() {  // lane 0
+  // lane 0: rows i_first-1, i_first into slots 12, 13 (2-row box)
+  __device__ __forceinline__ void issue_prologue() {
     const uint32_t bar = bar_s + 16u;
     mbar_expect_tx(bar, 2 * ROWB);
-    bulk_g2s(ring_s + 10 * ROWB, gsrc, ROWB, bar);
-    bulk_g2s(ring_s + 11 * ROWB, gsrc + pitch, ROWB, bar);
+    tma_rows(ring_s + 12 * ROWB, tm2, tm_x, tm_y, bar);
+  }
+  // this lane's NC values of one row in a ring slot
+  __device__ __forceinline__ void ld_row(const R* row, R (&x)[NC]) { ldsN<NC>(row + NC * lane, x); }
+
+  // Handoff ring layout [batch][step][16-B chunk][lane]: a warp's access to
+  // one chunk is 512 contiguous bytes (no bank conflicts).
+  __device__ __forceinline__ void hand_st(R* hp, int M6, const R (&x)[NC]) {
+#pragma unroll
+    for (int k = 0; k < NC / CH; ++k) {
+      R* q = hp + ((M6 * (NC / CH) + k) * 32 + lane) * CH;
+      if (sizeof(R) == 8)
+        *reinterpret_cast<double2*>(q) = make_double2((double)x[2 * k], (double)x[2 * k + 1]);
+      else
+        *reinterpret_cast<float4*>(q) = make_float4((float)x[4 * k], (float)x[4 * k + 1], (float)x[4 * k + 2], (float)x[4 * k + 3]);
+    }
+  }
+  __device__ __forceinline__ void hand_ld(const R* hp, int M6, R (&x)[NC]) {
+#pragma unroll
+    for (int k = 0; k < NC / CH; ++k) {
+      const R* q = hp + ((M6 * (NC / CH) + k) * 32 + lane) * CH;
+      if (sizeof(R) == 8) {
+        const double2 v = *reinterpret_cast<const double2*>(q);
+        x[2 * k] = (R)v.x;
+        x[2 * k + 1] = (R)v.y;
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(q);
+        x[4 * k] = (R)v.x; x[4 * k + 1] = (R)v.y; x[4 * k + 2] = (R)v.z; x[4 * k + 3] = (R)v.w;
+      }
+    }
   }
 
   template <int MK, int M6>
-  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, R* hp, long long c0) {
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp, R* hp) {
     constexpr int O = M6 & 1;
     constexpr int PH = M6 % 3;          // slot of age 0 (this step)
     constexpr int P1 = (PH + 2) % 3;    // age 1
     constexpr int P2 = (PH + 1) % 3;    // age 2
     if (SB == 0) {
-      lds4(rowp + M6 * kWaveCols, F[P1]);  // source row i+1 (ring slot (m+2)%3)
+      ld_row(rowp + M6 * WC, F[P1]);  // source row i+1
     } else {
-      // stages SB-1 (row i-SB+1) and SB-2 (row i-SB+2) of this step, from the front warp
-      R x[4];
-      lds4(hp + (M6 * 32 + lane) * 4, x);
-      C[SB - 1][PH][0] = x[0];
-      C[SB - 1][PH][1] = x[1];
-      C[SB - 2][PH][0] = x[2];
-      C[SB - 2][PH][1] = x[3];
+      // stage SB-1's row i-SB+1 of this step, stage SB-2's row i-SB of two
+      // steps ago (used only as the old value of stage SB's cells)
+      R x[NC];
+      hand_ld(hp, M6, x);
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        C[SB - 1][PH][h] = x[h];
+        if (SB >= 2) C[SB >= 2 ? SB - 2 : 0][P2][h] = x[NH + h];
+      }
     }
     // CK 3: bit s set iff stage s's row i-s is owned (R0 <= i-s < R1)
     unsigned int rowm = 0u;
@@ -521,107 +598,130 @@ struct WavePipe {
 #pragma unroll
     for (int s = SB; s < SE; ++s) {
       const int r = i - s;
-      R n0, n1, s0, s1, w0, w1, u0, u1;
-      if (s == 0) {
-        n0 = F[PH][O]; n1 = F[PH][O + 2];          // row i-1
-        s0 = F[P1][O]; s1 = F[P1][O + 2];          // row i+1
-        w0 = F[P2][1 - O]; w1 = F[P2][3 - O];      // row i, other colour
-        u0 = F[P2][O]; u1 = F[P2][O + 2];          // row i, self
-      } else {
-        const int p = s > 0 ? s - 1 : 0;
-        n0 = C[p][P2][0]; n1 = C[p][P2][1];        // row r-1
-        s0 = C[p][PH][0]; s1 = C[p][PH][1];        // row r+1
-        w0 = C[p][P1][0]; w1 = C[p][P1][1];        // row r
-        if (s == 1) {
-          u0 = F[PH][O]; u1 = F[PH][O + 2];        // source row i-1
+      R n[NH], sv[NH], w[NH], u[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        if (s == 0) {
+          n[h] = F[PH][O + 2 * h];          // row i-1
+          sv[h] = F[P1][O + 2 * h];         // row i+1
+          w[h] = F[P2][1 - O + 2 * h];      // row i, other colour
+          u[h] = F[P2][O + 2 * h];          // row i, self
         } else {
-          const int pp = s >= 2 ? s - 2 : 0;
-          u0 = C[pp][P2][0]; u1 = C[pp][P2][1];
+          const int p = s > 0 ? s - 1 : 0;
+          n[h] = C[p][P2][h];               // row r-1
+          sv[h] = C[p][PH][h];              // row r+1
+          w[h] = C[p][P1][h];               // row r
+          if (s == 1) {
+            u[h] = F[PH][O + 2 * h];        // source row i-1
+          } else {
+            const int pp = s >= 2 ? s - 2 : 0;
+            u[h] = C[pp][P2][h];
+          }
         }
       }
-      // W/E neighbour outside the lane: q=-1 (left lane's q=3) when O=0,
-      // q=4 (right lane's q=0) when O=1
-      const R nb = (O == 0) ? shfl_up1(w1) : shfl_dn1(w0);
-      const R mid = radd(w0, w1);
-      const R weA = (O == 0) ? radd(nb, w0) : mid;
-      const R weB = (O == 0) ? mid : radd(w1, nb);
-      R v0 = sor_update(radd(n0, s0), weA, u0, a.w);
-      R v1 = sor_update(radd(n1, s1), weB, u1, a.w);
-      if (MK == 1) {
-        v0 = upd[O] ? v0 : u0;
-        v1 = upd[O + 2] ? v1 : u1;
-      } else if (MK == 2) {
-        const bool rowok = (unsigned)(r - 1) < (unsigned)rows;
-        v0 = (rowok && upd[O]) ? v0 : u0;
-        v1 = (rowok && upd[O + 2]) ? v1 : u1;
+      // W/E neighbours of cell q = O+2h are the other colour's h-1, h (O = 0)
+      // or h, h+1 (O = 1); the one outside the lane is the left lane's last
+      // (O = 0) or the right lane's first (O = 1)
+      const R nb = (O == 0) ? shfl_up1(w[NH - 1]) : shfl_dn1(w[0]);
+      R v[NH], pcor[NH];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        const R we = (O == 0) ? radd(h == 0 ? nb : w[h > 0 ? h - 1 : 0], w[h])
+                              : radd(w[h], h == NH - 1 ? nb : w[h < NH - 1 ? h + 1 : 0]);
+        v[h] = sor_update_p(radd(n[h], sv[h]), we, u[h], a.w, pcor[h]);
+        if (MK == 1) {
+          v[h] = upd[O + 2 * h] ? v[h] : u[h];
+        } else if (MK == 2) {
+          const bool rowok = (unsigned)(r - 1) < (unsigned)rows;
+          v[h] = (rowok && upd[O + 2 * h]) ? v[h] : u[h];
+        }
       }
       if (CK == 4 && probe_row(M6, s)) {
         // probe rows of this batch: row i_first+6j (M6 == s) or 6 rows above
         // (M6 == s-6); their ownership masks are set once per batch
         const int pi = M6 < s ? 1 : 0;
-        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & ownA & pf[pi];
-        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & ownB & pf[pi];
-        hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
+#pragma unroll
+        for (int h = 0; h < NH; h += 2) {
+          const unsigned int hA = (unsigned int)hi_bits(rsub(v[h], u[h])) & ownM[h] & pf[pi];
+          const unsigned int hB =
+              h + 1 < NH ? (unsigned int)hi_bits(rsub(v[h + 1 < NH ? h + 1 : 0], u[h + 1 < NH ? h + 1 : 0])) &
+                               ownM[h + 1 < NH ? h + 1 : 0] & pf[pi]
+                         : 0u;
+          hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
+        }
       } else if (CK == 3) {
         // all-ones iff this stage's row is an owned row (bit s of rowm)
         const unsigned int fill = (unsigned int)((int)(rowm << (31 - s)) >> 31);
-        const unsigned int hA = (unsigned int)hi_bits(rsub(v0, u0)) & ownA & fill;
-        const unsigned int hB = (unsigned int)hi_bits(rsub(v1, u1)) & ownB & fill;
-        hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
+#pragma unroll
+        for (int h = 0; h < NH; h += 2) {
+          const unsigned int hA = (unsigned int)hi_bits(rsub(v[h], u[h])) & ownM[h] & fill;
+          const unsigned int hB =
+              h + 1 < NH ? (unsigned int)hi_bits(rsub(v[h + 1 < NH ? h + 1 : 0], u[h + 1 < NH ? h + 1 : 0])) &
+                               ownM[h + 1 < NH ? h + 1 : 0] & fill
+                         : 0u;
+          hmax[s >> 1] = max3u(hmax[s >> 1], hA, hB);
+        }
       } else if (CK != 0 && (CK == 2 || s >= S - 2)) {
         const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
         const int slot = CK == 2 ? (s >> 1) : 0;
-        const unsigned long long d0 = delta_bits(v0, u0), d1 = delta_bits(v1, u1);
-        dmax[slot] = umax64(dmax[slot], (inb && ownP[0]) ? d0 : 0ull);
-        dmax[slot] = umax64(dmax[slot], (inb && ownP[1]) ? d1 : 0ull);
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          dmax[slot] = umax64(dmax[slot], (inb && ownP[h]) ? delta_bits(v[h], u[h]) : 0ull);
       }
+      (void)pcor;
       if (s < S - 1) {
-        C[s][PH][0] = v0;
-        C[s][PH][1] = v1;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) C[s][PH][h] = v[h];
       } else {
-        // finished row r: this stage's colour at q = O, O+2; the other colour
-        // from stage S-2's row r (one step old, at q = 1-O, 3-O)
+        // finished row r: this stage's colour at q = O+2h; the other colour
+        // from stage S-2's row r (one step old, at q = 1-O+2h)
         const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
-        R out[4];
-        out[O] = v0;
-        out[O + 2] = v1;
-        out[1 - O] = C[S - 2][P1][0];
-        out[3 - O] = C[S - 2][P1][1];
-        if (T % 2 == 0) {  // ghost bands are whole lanes
-          stg4_if(inb && ownP[0], orow, out);
+        R out[NC];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          out[O + 2 * h] = v[h];
+          out[1 - O + 2 * h] = C[S - 2][P1][h];
+        }
+        if (LANE_OWN && NC % 4 == 0 && sizeof(R) == 8) {
+#pragma unroll
+          for (int k = 0; k < NC / 4; ++k)
+            stg4_if(inb && ownP[0], orow + 4 * k, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+        } else if (LANE_OWN && NC % 4 == 0) {
+#pragma unroll
+          for (int k = 0; k < NC / 4; ++k)
+            stg4_if(inb && ownP[0], orow + 4 * k, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
         } else {
-          stg2_if(inb && ownP[0], orow, out[0], out[1]);
-          stg2_if(inb && ownP[1], orow + 2, out[2], out[3]);
+#pragma unroll
+          for (int h = 0; h < NH; ++h) stg2_if(inb && ownP[h], orow + 2 * h, out[2 * h], out[2 * h + 1]);
         }
         orow += pitch;
       }
     }
     if (SE < S) {
-      R x[4] = {C[SE - 1][PH][0], C[SE - 1][PH][1], C[SE - 2][PH][0], C[SE - 2][PH][1]};
-      R* q = hp + (M6 * 32 + lane) * 4;
-      if (sizeof(R) == 8) {
-        reinterpret_cast<double2*>(q)[0] = make_double2((double)x[0], (double)x[1]);
-        reinterpret_cast<double2*>(q)[1] = make_double2((double)x[2], (double)x[3]);
-      } else {
-        *reinterpret_cast<float4*>(q) = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+      R x[NC];
+#pragma unroll
+      for (int h = 0; h < NH; ++h) {
+        x[h] = C[SE - 1][PH][h];
+        x[NH + h] = C[SE >= 2 ? SE - 2 : 0][P2][h];
       }
+      hand_st(hp, M6, x);
     }
   }
 
   template <int MK>
-  __device__ __forceinline__ void batch(const WaveArgs<R>& a, int i, const R* rowp, R* hp, long long c0) {
-    step<MK, 0>(a, i, rowp, hp, c0);
-    step<MK, 1>(a, i + 1, rowp, hp, c0);
-    step<MK, 2>(a, i + 2, rowp, hp, c0);
-    step<MK, 3>(a, i + 3, rowp, hp, c0);
-    step<MK, 4>(a, i + 4, rowp, hp, c0);
-    step<MK, 5>(a, i + 5, rowp, hp, c0);
+  __device__ __forceinline__ void batch(const WaveArgs<R>& a, int i, const R* rowp, R* hp) {
+    step<MK, 0>(a, i, rowp, hp);
+    step<MK, 1>(a, i + 1, rowp, hp);
+    step<MK, 2>(a, i + 2, rowp, hp);
+    step<MK, 3>(a, i + 3, rowp, hp);
+    step<MK, 4>(a, i + 4, rowp, hp);
+    step<MK, 5>(a, i + 5, rowp, hp);
   }
 
   // Batches [j0, j1) with masking level MK (one loop per level, so each loop
   // keeps its own register assignment and no value is moved between levels).
   template <int MK>
-  __device__ __forceinline__ void run_range(const WaveArgs<R>& a, int i_first, long long c0, int j0, int j1) {
+  __device__ __forceinline__ void run_range(const WaveArgs<R>& a, int i_first, int j0, int j1) {
     constexpr bool front = SB == 0;
     constexpr bool split = !(front && SE == S);
 #pragma unroll 1
@@ -634,15 +734,15 @@ struct WavePipe {
         pf[1] = (unsigned)(rp - 6 - R0) < (unsigned)(R1 - R0) ? 0xffffffffu : 0u;
       }
       const R* rowp = nullptr;
-      R* hp = split ? hand + (j & 1) * (6 * 32 * 4) : nullptr;
+      R* hp = split ? hand + (j & 1) * (6 * 32 * NC) : nullptr;
       if (front) {
         mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
-        rowp = ring + (j & 1) * 6 * kWaveCols + 4 * lane;
+        rowp = ring + (j & 1) * 6 * WC;
         if (split) named_bar_sync(bar_empty + (j & 1), 64);
       } else {
         named_bar_sync(bar_full + (j & 1), 64);
       }
-      batch<MK>(a, i_first + m, rowp, hp, c0);
+      batch<MK>(a, i_first + m, rowp, hp);
       if (front) {
         if (split) named_bar_arrive(bar_full + (j & 1), 64);
         __syncwarp();
@@ -655,7 +755,7 @@ struct WavePipe {
     }
   }
 
-  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first, long long c0) {
+  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first) {
     constexpr bool front = SB == 0, back = SE == S;
     constexpr bool split = !(front && back);
     if (split && !front) {  // back warp: both handoff buffers start empty
@@ -667,21 +767,23 @@ struct WavePipe {
     // masking.  The first and last batches of the top/bottom bands mask rows.
     const int jA = min(nbatch, max(0, -floordiv6(i_first - S)));            // ceil((S - i_first) / 6)
     const int jB = max(jA, min(nbatch, floordiv6(rows - 5 - i_first) + 1));
-    run_range<2>(a, i_first, c0, 0, jA);
+    run_range<2>(a, i_first, 0, jA);
     if (col_mask)
-      run_range<1>(a, i_first, c0, jA, jB);
+      run_range<1>(a, i_first, jA, jB);
     else
-      run_range<0>(a, i_first, c0, jA, jB);
-    run_range<2>(a, i_first, c0, jB, nbatch);
+      run_range<0>(a, i_first, jA, jB);
+    run_range<2>(a, i_first, jB, nbatch);
   }
 };
 
 // One warp (or warp pair) = one (strip, band) tile; tiles never synchronise.
-template <typename R, int T, int NST, int CK, int SB, int SE>
-__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMap* tm, unsigned char* wbase, R* hand, int bar_id,
-                                          int lane, int sw, int R0, int R1, int i_first, int nsteps,
+template <typename R, int T, int NST, int CK, int SB, int SE, int NC>
+__device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMap* tm, unsigned char* wbase, R* hand,
+                                          int bar_id, int lane, int sw, int R0, int R1, int i_first, int nsteps,
                                           unsigned long long (&dm)[kMaxT]) {
-  WavePipe<R, T, NST, CK, SB, SE> P;
+  using Pipe = WavePipe<R, T, NST, CK, SB, SE, NC>;
+  constexpr int WC = Pipe::WC, NH = Pipe::NH;
+  Pipe P;
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) {
     if (CK == 1 || CK == 2) P.dmax[t] = 0ull;
@@ -689,8 +791,8 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMa
   }
   P.ring = reinterpret_cast<const R*>(wbase);
   P.ring_s = smem_u32(wbase);
-  P.bar_s = P.ring_s + NST * kWaveCols * sizeof(R);
-  static_assert(NST == 12, "ring layout: 2 batches of 6 rows");
+  P.bar_s = P.ring_s + NST * WC * sizeof(R);
+  static_assert(NST == 14, "ring layout: 2 batches of 6 rows + 2 prologue rows");
   P.hand = hand;
   P.bar_full = bar_id;
   P.bar_empty = bar_id + 2;
@@ -698,38 +800,41 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMa
   P.rows = (int)a.rows;
   P.R0 = R0;
   P.R1 = R1;
-  const long long c0 = (long long)sw + 4 * lane;
+  const long long c0 = (long long)sw + NC * lane;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NC; ++q) {
     const int c = (int)c0 + q;
     P.upd[q] = (c >= 1) && (c <= (int)a.cols);
   }
-  P.col_mask = (sw >= 1 && sw + kWaveCols - 1 <= (int)a.cols) ? 0 : 1;
+  P.col_mask = (sw >= 1 && sw + WC - 1 <= (int)a.cols) ? 0 : 1;
   // Ownership by position: the strip minus its 2T ghost columns per side.
-  // The ghost bands are 2T wide and start at multiples of 4, so they cover
-  // whole column pairs (whole lanes for even T); cell A (q = O) is in pair 0,
-  // cell B (q = O+2) in pair 1.  Owned-by-position columns of different strips
-  // are disjoint.  Ring and padding columns inside it are never updated: they
-  // carry their source value through every stage, so storing them rewrites
-  // the value they hold and their |delta| is 0.  Stores and maxima therefore
-  // need no per-column test against [1, cols].
+  // The ghost bands are 2T wide and strips start at even columns, so they
+  // cover whole column pairs (q = 2h, 2h+1; whole lanes when NC divides 2T);
+  // cell q = O+2h is in pair h.  Owned-by-position columns of different
+  // strips are disjoint.  Ring and padding columns inside it are never
+  // updated: they carry their source value through every stage, so storing
+  // them rewrites the value they hold and their |delta| is 0.  Stores and
+  // maxima therefore need no per-column test against [1, cols].
   {
-    const int g_lo = sw + 2 * T, g_hi = sw + kWaveCols - 2 * T;
-    const int cA = (int)c0, cB = (int)c0 + 2;
-    P.ownP[0] = cA >= g_lo && cA + 1 < g_hi;
-    P.ownP[1] = cB >= g_lo && cB + 1 < g_hi;
-    P.ownA = P.ownP[0] ? 0x7fffffffu : 0u;
-    P.ownB = P.ownP[1] ? 0x7fffffffu : 0u;
+    const int g_lo = sw + 2 * T, g_hi = sw + WC - 2 * T;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      const int cp = (int)c0 + 2 * h;
+      P.ownP[h] = cp >= g_lo && cp + 1 < g_hi;
+      P.ownM[h] = P.ownP[h] ? 0x7fffffffu : 0u;
+    }
   }
   // row finished by stage S-1 at step 0 is i_first - (S-1)
   P.orow = a.dst + (long long)(i_first - (2 * T - 1) - a.g0) * a.pitch + c0;
 #pragma unroll
   for (int s = 0; s < 2 * T - 1; ++s)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) P.C[s][k][0] = P.C[s][k][1] = R(0);
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int h = 0; h < NH; ++h) P.C[s][k][h] = R(0);
   P.pitch = a.pitch;
-  P.gsrc = a.src + (long long)(i_first - 1 - a.g0) * a.pitch + sw;
   P.tm = tm;
+  P.tm2 = tm + 1;
   P.tm_x = kColPad + sw;
   P.tm_y = i_first - 1 - (int)a.g0;
   P.nbatch = nsteps / 6;
@@ -742,43 +847,43 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMa
     __syncwarp();
     if (lane == 0) {
       P.issue_prologue();
-      P.issue_batch(0);
-      if (P.nbatch > 1) P.issue_batch(1, 0, 4);
+      P.issue_batch_tma(0);
+      if (P.nbatch > 1) P.issue_batch_tma(1);
     }
     mbar_wait(P.bar_s + 16u, 0u);
-    lds4(P.ring + 10 * kWaveCols + 4 * lane, P.F[0]);  // row i_first - 1
-    lds4(P.ring + 11 * kWaveCols + 4 * lane, P.F[1]);  // row i_first
-    __syncwarp();
-    if (lane == 0 && P.nbatch > 1) {
-      fence_proxy_async_smem();
-      P.issue_batch(1, 4, 6);
-    }
+    P.ld_row(P.ring + 12 * WC, P.F[0]);  // row i_first - 1
+    P.ld_row(P.ring + 13 * WC, P.F[1]);  // row i_first
   }
-  P.run(a, i_first, c0);
+  P.run(a, i_first);
 #pragma unroll
   for (int t = 0; t < P.NSLOT; ++t) dm[t] = CK >= 3 ? (unsigned long long)P.hmax[t] : P.dmax[(CK == 1 || CK == 2) ? t : 0];
 }
 
-// Register budget: >= 3 resident CTAs (12 warps) per SM for deep pipelines;
-// split kernels hold half the stages per warp and aim for 4 CTAs.
+// Register budget per configuration: resident CTAs (4 warps each) per SM.
+// NC = 4: split kernels hold half the stages per warp and aim for 4 CTAs;
+// wider lanes hold NC/4 times the registers and trade warps for ILP.
 #ifndef SOR_WAVE_MINB34
 #define SOR_WAVE_MINB34 3
 #endif
-__host__ __device__ constexpr int wave_min_blocks(int T, bool split) {
-  return split ? 4 : (T <= 2 ? 4 : SOR_WAVE_MINB34);
+#ifndef SOR_WAVE_MINB_SPLIT
+#define SOR_WAVE_MINB_SPLIT 4
+#endif
+__host__ __device__ constexpr int wave_min_blocks(int T, bool split, int NC) {
+  return NC == 8 ? 2 : NC == 6 ? 3 : split ? SOR_WAVE_MINB_SPLIT : (T <= 2 ? 4 : SOR_WAVE_MINB34);
 }
 // warps (tiles, or warp pairs in split mode) per CTA
 __host__ __device__ constexpr int wave_tiles_per_cta(bool split) { return split ? kWaveWarps / 2 : kWaveWarps; }
-template <typename R, int NST, bool SPLIT>
+template <typename R, int NST, bool SPLIT, int NC>
 __host__ __device__ constexpr int wave_smem_bytes() {
-  return SPLIT ? (kWaveWarps / 2) * wave_smem_per_pair<R, NST>() : kWaveWarps * wave_smem_per_warp<R, NST>();
+  return SPLIT ? (kWaveWarps / 2) * wave_smem_per_pair<R, NST, NC>() : kWaveWarps * wave_smem_per_warp<R, NST, NC>();
 }
 
-template <typename R, int T, int NST, int CK, bool SPLIT>
-__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
-    wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ CUtensorMap tm) {
+template <typename R, int T, int NST, int CK, bool SPLIT, int NC>
+__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
+    wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
   extern __shared__ __align__(128) unsigned char wave_smem[];
+  constexpr int WC = wave_cols<NC>();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
@@ -787,7 +892,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
   unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
   if (gw < a.ntiles) {
     const int4 tile = a.tiles[gw];
-    const int sw = a.s0 + tile.x * (kWaveCols - 4 * T);
+    const int sw = a.s0 + tile.x * (WC - 4 * T);
     const int R0 = tile.y;
     const int R1 = tile.z;
     // step m (front row i_first+m) feeds stage 2T-1 row i_first+m-2T+1;
@@ -795,16 +900,16 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT))
     const int i_first = (R0 - (2 * T - 1)) & ~1;
     const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
     if (SPLIT) {
-      unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST>();
-      R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST>());
+      unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST, NC>();
+      R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST, NC>());
       const int bar_id = 1 + 4 * slot;  // named barriers 1..8 (0 is __syncthreads)
       if (role == 0)
-        wave_tile<R, T, NST, CK, 0, T>(a, &tm, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, 0, T, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
       else
-        wave_tile<R, T, NST, CK, T, 2 * T>(a, &tm, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, T, 2 * T, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
     } else {
-      unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST>();
-      wave_tile<R, T, NST, CK, 0, 2 * T>(a, &tm, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+      unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
+      wave_tile<R, T, NST, CK, 0, 2 * T, NC>(a, tm.m, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
     }
   }
   (void)role;
