@@ -39,8 +39,10 @@ struct Slab {
   int64_t g_lo = 0, g_hi = 0;  // owned global interior rows [g_lo, g_hi)
   int64_t g0 = 0;              // global row of storage row 0 (= g_lo - kRowPad)
   int64_t nstore = 0;          // storage rows
-  void* plane[2] = {nullptr, nullptr};
-  WaveMaps tmap[2];  // per plane: tensor maps of the wave kernel's source-row boxes
+  // planes 0, 1: ping-pong; plane 2 (allocated on the first deferred solve):
+  // the speculative pass of the deferred stop test writes the third plane
+  void* plane[3] = {nullptr, nullptr, nullptr};
+  WaveMaps tmap[3];  // per plane: tensor maps of the wave kernel's source-row boxes
 };
 
 enum class Mode { Single, Virtual, Dist };
@@ -75,7 +77,18 @@ struct sor_grid {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   int halo_valid = kRowPad;  // rows of the current plane's halos known up to date
-  std::vector<std::pair<int64_t, std::pair<int, int>>> pass_ends;
+  struct PassRec {
+    int64_t k_last;
+    int src, dst, T;
+  };
+  std::vector<PassRec> pass_ends;  // wave passes of the current solve segment
+  int nplanes = 2;                 // planes in rotation (3 once the deferred solve allocated plane 2)
+  int nxt(int p) const { return (p + 1) % nplanes; }
+  // deferred stop test: the last checked pass not yet decided, and the slot set
+  // the next checked pass contributes to
+  bool prev_valid = false;
+  int prev_T = 0, prev_ck = 0, prev_set = 0, next_set = 0;
+  int64_t prev_k_last = 0;
   // wave-kernel tile tables per (slab, T, occupancy): device int4 array + count
   std::map<std::tuple<int, int, int>, std::pair<int4*, int>> tiles;  // (last iteration, (cur after, T))
   int64_t exact_reruns = 0;  // solve passes re-run with exact maxima (diagnostic)
@@ -242,7 +255,8 @@ int load_all(sor_grid* g, const double* init) {
     const int64_t ga = std::max<int64_t>(0, s.g0);
     const int64_t gb = std::min<int64_t>(g->rows + 2, s.g0 + s.nstore);
     TRY(load_rows(g, s, 0, init, ga, gb));
-    CU(cudaMemcpyAsync(s.plane[1], s.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
+    for (int p = 1; p < 3; ++p)
+      if (s.plane[p]) CU(cudaMemcpyAsync(s.plane[p], s.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
   }
   g->cur = 0;
   g->halo_valid = kRowPad;
@@ -262,7 +276,7 @@ int validate_dims(int64_t rows, int64_t cols) {
 void free_grid(sor_grid* g) {
   if (!g) return;
   for (auto& s : g->slabs)
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < 3; ++p)
       if (s.plane[p]) cudaFree(s.plane[p]);
   if (g->dstate) cudaFree(g->dstate);
   if (g->hstate) cudaFreeHost(g->hstate);
@@ -625,6 +639,14 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
   return SOR_OK;
 }
 
+// Programmatic dependent launch between consecutive wave kernels (one slab:
+// no NCCL or copy between them); SOR_NO_PDL=1 disables it.
+bool wave_pdl(const sor_grid* g) {
+  static int off = -1;
+  if (off < 0) off = getenv("SOR_NO_PDL") ? 1 : 0;
+  return !off && g->slabs.size() == 1 && g->nranks == 1;
+}
+
 // Split mode (a warp pair per tile, stages divided between the two warps) for
 // T >= 2 unless SOR_WAVE_SPLIT=0.
 bool wave_split(int T) {
@@ -649,7 +671,7 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   }
   WaveArgs<R> a;
   a.src = col0<R>(s.plane[g->cur]);
-  a.dst = col0<R>(s.plane[g->cur ^ 1]);
+  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
   a.pitch = g->pitch;
   a.g0 = s.g0;
   a.rows = g->rows;
@@ -663,12 +685,23 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   TRY(wave_tiles(g, s, slab_idx, T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
   a.tiles = tt.first;
   a.ntiles = tt.second;
-  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta);
+  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta) + (ctl.defer ? 1 : 0);
   IterCtl c = ctl;
   c.finalize = fused_fin ? 1 : 0;
   c.nparts = blocks;
-  wave_kernel<R, T, NST, CK, SPLIT, NC><<<blocks, kWaveWarps * 32, smem, g->stream>>>(a, c, s.tmap[g->cur]);
-  CU(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // PDL only for one-wave launches: in a multi-wave launch the next grid's
+  // early CTAs would hold slots its own tail needs (measured: C5 -0.5%, C3 +2%)
+  cfg.numAttrs = (wave_pdl(g) && blocks <= (unsigned)(occ * g->nsm)) ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC>, a, c, s.tmap[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
@@ -697,7 +730,7 @@ int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool
 template <typename R>
 int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   const int T = ctl.T;
-  const bool fused_fin = single_part(g) && ctl.ck != 0;
+  const bool fused_fin = single_part(g) && ctl.ck != 0 && !ctl.defer;
   if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
   for (auto& s : g->slabs) {
     if (ctl.ck == 4)
@@ -711,13 +744,14 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
     else
       TRY((launch_wave<R, 0>(g, s, T, w, ctl, fused_fin)));
   }
-  g->cur ^= 1;
+  const int src = g->cur;
+  g->cur = g->nxt(src);
   g->st.half_sweeps += 2 * T;
   g->st.hbm_passes += 1;
   TRY(exchange(g, g->cur, 2 * T));
   g->halo_valid = 2 * T;
-  if (ctl.ck && !fused_fin) TRY(join_and_finalize(g, ctl));
-  g->pass_ends.push_back({ctl.k_last, {g->cur, T}});
+  if (ctl.ck && !fused_fin && !ctl.defer) TRY(join_and_finalize(g, ctl));
+  g->pass_ends.push_back({ctl.k_last, src, g->cur, T});
   return SOR_OK;
 }
 
@@ -818,6 +852,24 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
       c.k_last = k + t - 1;
       c.T = t;
       c.ck = every ? g->every_ck : (c.k_last == next_check ? 1 : 0);
+      if (base.defer) {
+        // this launch's block 0 decides the last undecided checked pass
+        c.prev_valid = g->prev_valid ? 1 : 0;
+        c.prev_k_last = g->prev_k_last;
+        c.prev_T = g->prev_T;
+        c.prev_ck = g->prev_ck;
+        c.prev_set = g->prev_set;
+        g->prev_valid = false;
+        c.set = g->next_set;
+        if (c.ck) {
+          g->prev_valid = true;
+          g->prev_k_last = c.k_last;
+          g->prev_T = c.T;
+          g->prev_ck = c.ck;
+          g->prev_set = c.set;
+          g->next_set ^= 1;
+        }
+      }
       TRY(wave_pass<R>(g, w, c));
       if (c.ck) g->st.checks += every ? t : 1;
       k += t;
@@ -857,13 +909,11 @@ int read_state(sor_grid* g, DevState* out) {
   return SOR_OK;
 }
 
-// The pass of this solve segment that contains iteration k: (k_end, cur after, depth).
-bool find_pass(const sor_grid* g, int64_t k, int64_t* k_end, int* cur_after, int* tp) {
+// The pass of this solve segment that contains iteration k.
+bool find_pass(const sor_grid* g, int64_t k, sor_grid::PassRec* out) {
   for (const auto& pe : g->pass_ends) {
-    if (k <= pe.first && k > pe.first - pe.second.second) {
-      *k_end = pe.first;
-      *cur_after = pe.second.first;
-      *tp = pe.second.second;
+    if (k <= pe.k_last && k > pe.k_last - pe.T) {
+      *out = pe;
       return true;
     }
   }
@@ -875,17 +925,43 @@ bool find_pass(const sor_grid* g, int64_t k, int64_t* k_end, int* cur_after, int
 // the exact max-change of its last iteration (ck=1) or of every iteration
 // (ck=2, solve semantics).  Leaves g->cur on the plane holding the result.
 template <typename R>
-int rerun_pass(sor_grid* g, R w, const IterCtl& base, int64_t k_end, int cur_after, int tp, int depth,
-               int ck, DevState* out) {
+int rerun_pass(sor_grid* g, R w, const IterCtl& base, const sor_grid::PassRec& pr, int depth, int ck, DevState* out) {
   CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
-  g->cur = cur_after ^ 1;
+  g->cur = pr.src;  // writes the pass's own destination plane again
   IterCtl c = base;
-  c.k_last = k_end - tp + depth;
+  c.k_last = pr.k_last - pr.T + depth;
   c.T = depth;
   c.ck = ck;
   c.solve = ck == 2 ? 1 : 0;
+  c.defer = 0;
+  c.set = 0;
   TRY(wave_pass<R>(g, w, c));
   return read_state(g, out);
+}
+
+// Third plane for the deferred stop test (single slab): allocated once, a copy
+// of the current plane (ring, padding); false if memory is short.
+bool ensure_third_plane(sor_grid* g) {
+  if (g->nplanes == 3) return true;
+  if (!single_part(g)) return false;
+  static int off = -1;
+  if (off < 0) off = getenv("SOR_NO_DEFER") ? 1 : 0;
+  if (off) return false;
+  Slab& s = g->slabs[0];
+  const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
+  if (cudaMalloc(&s.plane[2], bytes) != cudaSuccess) {
+    cudaGetLastError();
+    s.plane[2] = nullptr;
+    return false;
+  }
+  if (cudaMemcpyAsync(s.plane[2], s.plane[g->cur], bytes, cudaMemcpyDeviceToDevice, g->stream) != cudaSuccess ||
+      make_tmaps(g, s, 2) != SOR_OK) {
+    cudaFree(s.plane[2]);
+    s.plane[2] = nullptr;
+    return false;
+  }
+  g->nplanes = 3;
+  return true;
 }
 
 template <typename R>
@@ -917,6 +993,12 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
       base.tol_hi = (unsigned)(tb >> 32);
     }
     const bool fast = g->kernel != SOR_KERNEL_NATURAL && K == 1 && depth_of(g) > 1;  // ck=3/4 passes
+    // Deferred stop test (wave kernels, one slab): no ticket at the end of a
+    // checked pass; the next launch's block 0 decides it while the rest of
+    // that launch runs speculatively into the third plane, and the launch
+    // after exits early once a test stopped.  Pass p's source plane survives
+    // pass p+1 (three-plane rotation), so an exact re-run is always possible.
+    base.defer = (g->kernel != SOR_KERNEL_NATURAL && ensure_third_plane(g)) ? 1 : 0;
     // batches of whole check blocks (and whole passes); poll one batch behind
     const int64_t unit = std::max<int64_t>(K, depth_of(g));
     const int64_t blk = std::max<int64_t>(unit, (int64_t)((64 + unit - 1) / unit) * unit);
@@ -930,6 +1012,8 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
       // one segment: iterations k..maxit until the device stops the loop
       CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
       g->pass_ends.clear();
+      g->prev_valid = false;
+      g->next_set = 0;
       int b = 0;
       for (int64_t kk = k; kk <= maxit;) {
         const int64_t k_to = std::min(maxit, kk + blk - 1);
@@ -944,6 +1028,19 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         }
         ++b;
       }
+      if (base.defer && g->prev_valid) {
+        // the last enqueued checked pass has no successor to decide it
+        IterCtl c = base;
+        c.k_last = g->prev_k_last;
+        c.T = g->prev_T;
+        c.ck = g->prev_ck;
+        c.set = g->prev_set;
+        c.defer = 0;
+        finalize_kernel<<<1, 32, 0, g->stream>>>(c);
+        CU(cudaGetLastError());
+        g->st.kernel_launches += 1;
+        g->prev_valid = false;
+      }
       TRY(read_state(g, &hs));
       checks += hs.checks;
       if (g->kernel == SOR_KERNEL_NATURAL) {  // in place, exact checks: nothing to redo
@@ -952,25 +1049,24 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         maxc = hs.max_change;
         break;
       }
-      int64_t k_end = 0;
-      int cur_after = g->cur, tp = 1;
+      sor_grid::PassRec pr{};
       if (hs.ambiguous) {
         // ck=3: high words tied with tol's; ck=4: the probe could not exclude
         // convergence.  Decide this pass exactly
         g->exact_reruns += 1;
         if (getenv("SOR_DEBUG")) fprintf(stderr, "[sor] exact re-run at iteration %lld\n", (long long)hs.amb_iter);
-        if (!find_pass(g, hs.amb_iter, &k_end, &cur_after, &tp))
+        if (!find_pass(g, hs.amb_iter, &pr))
           return set_error(g, SOR_E_STATE, "internal: pass of iteration %lld not found", (long long)hs.amb_iter);
-        checks -= (hs.amb_iter - (k_end - tp + 1)) + 1;  // the exact pass re-counts them
+        checks -= (hs.amb_iter - (pr.k_last - pr.T + 1)) + 1;  // the exact pass re-counts them
         DevState ex{};
-        TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, tp, 2, &ex));
+        TRY(rerun_pass<R>(g, w, base, pr, pr.T, 2, &ex));
         if (ex.converged) {
           checks += ex.checks;
           converged = true;
           done = ex.conv_iter;
-          const int depth = (int)(done - (k_end - tp));
+          const int depth = (int)(done - (pr.k_last - pr.T));
           DevState fin{};
-          TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, depth, 1, &fin));
+          TRY(rerun_pass<R>(g, w, base, pr, depth, 1, &fin));
           maxc = fin.max_change;
           break;
         }
@@ -990,7 +1086,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
                     hs.max_change, ex.max_change, tol);
           if (ex.max_change < sw * tol) g->every_ck = 3;
         }
-        k = k_end + 1;  // g->cur now holds X_{k_end}
+        k = pr.k_last + 1;  // g->cur now holds X_{k_last}
         if (k > maxit) {
           done = maxit;
           break;
@@ -1003,15 +1099,15 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
       } else {
         done = maxit;
       }
-      if (!find_pass(g, done, &k_end, &cur_after, &tp))
+      if (!find_pass(g, done, &pr))
         return set_error(g, SOR_E_STATE, "internal: pass of iteration %lld not found", (long long)done);
       if (fast) {
         // X_done and its exact max-change: re-run the pass up to `done`
         DevState fin{};
-        TRY(rerun_pass<R>(g, w, base, k_end, cur_after, tp, (int)(done - (k_end - tp)), 1, &fin));
+        TRY(rerun_pass<R>(g, w, base, pr, (int)(done - (pr.k_last - pr.T)), 1, &fin));
         maxc = fin.max_change;
       } else {
-        g->cur = cur_after;  // passes end on checked iterations
+        g->cur = pr.dst;  // passes end on checked iterations
         maxc = hs.max_change;
       }
       break;

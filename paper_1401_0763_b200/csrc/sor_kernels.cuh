@@ -42,9 +42,10 @@ constexpr int kWaveNC = 4;     // columns per lane in wave_kernel (strip = 32*kW
 constexpr int kMaxT = 4;      // max temporal depth (iterations per HBM pass)
 
 struct DevState {
-  // ordered bits of max |delta| per iteration of a pass; one 128-B line each
+  // ordered bits of max |delta| per iteration of a pass, in two slot sets
+  // (consecutive passes of a deferred solve alternate); one 128-B line each
   // so the per-CTA atomics of different slots hit different L2 slices
-  unsigned long long maxbits[kMaxT][16];
+  unsigned long long maxbits[2][kMaxT][16];
   unsigned int ticket;         // finishing-part counter for the fused finalize
   int stop;                    // solve: converged or maxit reached -> later launches exit
   int converged;
@@ -72,8 +73,17 @@ struct IterCtl {
                         // proves "not converged" and anything else is resolved exactly
   unsigned int tol_hi;  // high 32 bits of tol (ck=3)
   int solve;            // apply the stop test / early exit
-  int finalize;         // this launch's last part runs the stop test
+  int finalize;         // this launch's last part runs the stop test (ticket)
   unsigned int nparts;  // number of ticket takers (warps or CTAs) in this launch
+  int set;              // maxbits slot set this launch contributes to
+  // Deferred stop test (wave kernel, single slab, solve): no ticket; block 0
+  // of this launch runs the stop test of the PREVIOUS pass (prev_*, slot set
+  // set^1) while the other blocks compute this pass speculatively into the
+  // third plane.  The launch after it exits early if that test stopped.
+  int defer;
+  int prev_valid;
+  int prev_T, prev_ck, prev_set;
+  long long prev_k_last;
 };
 
 __host__ __device__ __forceinline__ int floordiv6(int x) { return x >= 0 ? x / 6 : -((5 - x) / 6); }
@@ -131,25 +141,27 @@ __device__ __forceinline__ int ld_stop(const DevState* st) {
   return *reinterpret_cast<const volatile int*>(&st->stop);
 }
 
-// Stop test of Algorithm 1 [P:319-331] for the iterations of one pass; their
-// maxima are complete in st->maxbits[].  Strict '<' (reading #7).
-__device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) {
-  const long long k0 = ctl.k_last - (ctl.T - 1);
+// Stop test of Algorithm 1 [P:319-331] for the iterations of one pass (T
+// iterations ending at k_last, max-change mode ck); their maxima are complete
+// in st->maxbits[set].  Strict '<' (reading #7).
+__device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl, long long k_last, int T, int ck,
+                                              int set) {
+  const long long k0 = k_last - (T - 1);
   st->ticket = 0u;
-  for (int t = 0; t < ctl.T; ++t) {
+  for (int t = 0; t < T; ++t) {
     const long long k = k0 + t;
-    const bool every = ctl.ck >= 2;
+    const bool every = ck >= 2;
     const int slot = every ? t : 0;
-    const bool checked = every ? (!ctl.solve || k % ctl.K == 0) : (t == ctl.T - 1);
+    const bool checked = every ? (!ctl.solve || k % ctl.K == 0) : (t == T - 1);
     if (!checked) continue;
-    if (ctl.ck >= 3) {
+    if (ck >= 3) {
       // non-negative doubles order like their bit patterns: a smaller high
       // word decides '<', a larger one '>='; equal high words are ambiguous
-      const unsigned int h = (unsigned int)(st->maxbits[slot][0] >> 32);
+      const unsigned int h = (unsigned int)(st->maxbits[set][slot][0] >> 32);
       st->checks += 1;
       st->iters_done = k;
       st->max_change = __longlong_as_double((long long)((unsigned long long)h << 32));
-      if (ctl.ck == 4) {
+      if (ck == 4) {
         // probe max <= full max: only "probe > tol" is conclusive
         if (h <= ctl.tol_hi) {
           st->ambiguous = 1;
@@ -174,7 +186,7 @@ __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) 
       }
       continue;
     }
-    const double m = __longlong_as_double((long long)st->maxbits[slot][0]);
+    const double m = __longlong_as_double((long long)st->maxbits[set][slot][0]);
     st->checks += 1;
     st->max_change = m;
     st->iters_done = k;
@@ -186,14 +198,17 @@ __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) 
       break;
     }
   }
-  for (int t = 0; t < kMaxT; ++t) st->maxbits[t][0] = 0ull;
-  if (ctl.solve && ctl.k_last >= ctl.maxit) st->stop = 1;
+  for (int t = 0; t < kMaxT; ++t) st->maxbits[set][t][0] = 0ull;
+  if (ctl.solve && k_last >= ctl.maxit) st->stop = 1;
   __threadfence();
+}
+__device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) {
+  finalize_pass(st, ctl, ctl.k_last, ctl.T, ctl.ck, ctl.set);
 }
 
 // One part (warp or CTA) contributes its maxima; the last part finalizes.
 __device__ __forceinline__ void contribute(const IterCtl& ctl, int slot, unsigned long long bits) {
-  if (bits) atomicMax(&ctl.st->maxbits[slot][0], bits);
+  if (bits) atomicMax(&ctl.st->maxbits[ctl.set][slot][0], bits);
 }
 __device__ __forceinline__ void maybe_finalize(const IterCtl& ctl) {
   if (ctl.finalize) {
@@ -881,14 +896,34 @@ __host__ __device__ constexpr int wave_smem_bytes() {
 template <typename R, int T, int NST, int CK, bool SPLIT, int NC>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
     wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
-  if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  // Programmatic dependent launch (single slab): the next launch in the
+  // stream may be scheduled as soon as every CTA of this one has started;
+  // everything this launch reads (source plane, stop flag, maxima) is written
+  // by the previous launch, so wait for its completion first.  Both are no-ops
+  // for an ordinary launch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (ctl.st && ctl.solve) {
+    if (ctl.defer && blockIdx.x == 0) {  // the decision block: stop test of the previous pass
+      if (threadIdx.x == 0 && ctl.prev_valid && !ld_stop(ctl.st))
+        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set);
+      return;
+    }
+    // one read per CTA: with a deferred stop test the flag can change while
+    // this launch runs, and the warps of a pair must agree (named barriers)
+    __shared__ int cta_stop;
+    if (threadIdx.x == 0) cta_stop = ld_stop(ctl.st);
+    __syncthreads();
+    if (cta_stop) return;
+  }
+  const int bid = (int)blockIdx.x - ctl.defer;
   extern __shared__ __align__(128) unsigned char wave_smem[];
   constexpr int WC = wave_cols<NC>();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
   const int role = SPLIT ? warp & 1 : 0;      // 0 front (or whole), 1 back
-  const int gw = blockIdx.x * wave_tiles_per_cta(SPLIT) + slot;
+  const int gw = bid * wave_tiles_per_cta(SPLIT) + slot;
   unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
   if (gw < a.ntiles) {
     const int4 tile = a.tiles[gw];
