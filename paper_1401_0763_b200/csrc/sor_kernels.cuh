@@ -513,8 +513,10 @@ struct WavePipe {
   static constexpr int NSLOT = CK >= 2 ? T : 1;
   // ghost bands (2T columns) cover whole lanes: one ownership flag per lane
   static constexpr bool LANE_OWN = (2 * T) % NC == 0;
-  // CK 4 probes the rows with (row - i_first) % 6 == 0: in the 6-step
-  // unrolled loop that is the compile-time condition (M6 - s) % 6 == 0
+  // CK 4 probes the red stage (s even) of each iteration on the rows with
+  // (row - i_first) % 6 == 0: in the 6-step unrolled loop that is the
+  // compile-time condition (M6 - s) % 6 == 0.  A lower bound of the
+  // iteration's max-change, as the probe must be.
   __host__ __device__ static constexpr bool probe_row(int M6, int s) { return ((M6 - s) % 6 + 6) % 6 == 0; }
   R F[3][NC];                 // source rows, slot = (row - (i_first-1)) % 3 (front warp)
   R C[S - 1][3][NH];          // stage outputs, slot = step % 3 (unused stages vanish)
@@ -651,7 +653,7 @@ struct WavePipe {
           v[h] = (rowok && upd[O + 2 * h]) ? v[h] : u[h];
         }
       }
-      if (CK == 4 && probe_row(M6, s)) {
+      if (CK == 4 && (s & 1) == 0 && probe_row(M6, s)) {
         // probe rows of this batch: row i_first+6j (M6 == s) or 6 rows above
         // (M6 == s-6); their ownership masks are set once per batch
         const int pi = M6 < s ? 1 : 0;
@@ -886,6 +888,12 @@ __device__ __forceinline__ void wave_tile(const WaveArgs<R>& a, const CUtensorMa
 __host__ __device__ constexpr int wave_min_blocks(int T, bool split, int NC) {
   return NC == 8 ? 2 : NC == 6 ? 3 : split ? SOR_WAVE_MINB_SPLIT : (T <= 2 ? 4 : SOR_WAVE_MINB34);
 }
+// Split point of a warp pair: the front warp runs stages [0, K), the back
+// warp [K, 2T).  The front also streams the source rows (TMA waits, LDS) and
+// was measured to be the slower warp at K = T, so it gets fewer stages.
+// (Measured on B200, C3/C5: T = 4 -> K = 3 is 2-4% faster than K = 4, K = 2
+// slower; T = 3 -> K = 3 beats K = 2; T = 2 needs K = 2.)
+__host__ __device__ constexpr int wave_split_stage(int T) { return T == 4 ? 3 : T; }
 // warps (tiles, or warp pairs in split mode) per CTA
 __host__ __device__ constexpr int wave_tiles_per_cta(bool split) { return split ? kWaveWarps / 2 : kWaveWarps; }
 template <typename R, int NST, bool SPLIT, int NC>
@@ -938,10 +946,11 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
       unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST, NC>();
       R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST, NC>());
       const int bar_id = 1 + 4 * slot;  // named barriers 1..8 (0 is __syncthreads)
+      constexpr int K = wave_split_stage(T);
       if (role == 0)
-        wave_tile<R, T, NST, CK, 0, T, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, 0, K, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
       else
-        wave_tile<R, T, NST, CK, T, 2 * T, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        wave_tile<R, T, NST, CK, K, 2 * T, NC>(a, tm.m, pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
     } else {
       unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
       wave_tile<R, T, NST, CK, 0, 2 * T, NC>(a, tm.m, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);

@@ -8,6 +8,8 @@ the stated tolerances (fp64 <= 1e-12*max|bnd|, fp32 <= 1e-5 rel, iterations
 +-1).  Sizes span several warp strips (124..112 columns) and bands, with
 ragged tails, odd/even dimensions and degenerate 1-wide grids.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -253,3 +255,61 @@ def test_dist_single_rank_nccl(gpu, orc, kernel, T):
     assert (st["rank"], st["nranks"]) == (0, 1)
     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("T", [1, 2, 3, 4])
+def test_deferred_solve_repeated_on_one_handle(gpu, orc, T):
+    """Deferred stop test: the stop flag changes while a launch runs; repeated
+    solves (reset in between), iterate/solve alternation and a re-run after an
+    inconclusive probe all keep the oracle's iteration count and grid."""
+    init = SI.random_edges(300, 517, seed=40 + T)
+    ref = init.copy()
+    rr = orc.solve(ref, 1.95, 1e-7, 20000, 1)
+    with gpu.Grid.create(init) as g:
+        g.set_kernel("temporal" if T > 1 else "fused", T)
+        for _ in range(3):
+            g.reset(init)
+            r = g.solve(1.95, 1e-7, 20000, 1)
+            assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
+            assert np.array_equal(g.download(), ref)
+        # continuation: a few more iterations, then a tighter solve on the same handle
+        ref2 = ref.copy()
+        orc.iterate(ref2, 1.95, 7)
+        rr2 = orc.solve(ref2, 1.95, 1e-9, 20000, 1)
+        g.iterate(1.95, 7)
+        r2 = g.solve(1.95, 1e-9, 20000, 1)
+        assert (r2.converged, r2.iters, r2.max_change) == (rr2.converged, rr2.iters, rr2.max_change)
+        assert np.array_equal(g.download(), ref2)
+
+
+_SUBPROC = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, sor_inputs as SI, paper_1401_0763_b200 as P
+cfg = SI.config("C1")
+ref = cfg.init(); rr = oracle.solve(ref, cfg.omega, cfg.tol, cfg.maxit, 1)
+for kernel, T in (("fused", 1), ("temporal", 2), ("temporal", 4)):
+    with P.Grid.create(cfg.init()) as g:
+        g.set_kernel(kernel, T)
+        r = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1)
+        assert (r.iters, r.max_change) == (rr.iters, rr.max_change), (kernel, T, r, rr.iters)
+        assert np.array_equal(g.download(), ref), (kernel, T)
+init = SI.random_edges(97, 260, seed=5)
+ref = init.copy(); oracle.iterate(ref, 1.8, 9)
+with P.Grid.create(init) as g:
+    g.set_kernel("temporal", 3); g.iterate(1.8, 9)
+    assert np.array_equal(g.download(), ref)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", ["SOR_NO_DEFER", "SOR_NO_PDL"])
+def test_fallback_paths_in_subprocess(gpu, env):
+    """The two-plane ticket stop test (used when the third plane cannot be
+    allocated) and ordinary launches (no PDL) give the same results."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **{env: "1"})
+    r = subprocess.run([sys.executable, "-c", _SUBPROC % root], env=e, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
