@@ -911,6 +911,9 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
   // for an ordinary launch.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the previous launch wrote the source plane through the generic proxy;
+  // this launch reads it with TMA (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   if (ctl.st && ctl.solve) {
     if (ctl.defer && blockIdx.x == 0) {  // the decision block: stop test of the previous pass
       if (threadIdx.x == 0 && ctl.prev_valid && !ld_stop(ctl.st))

@@ -284,6 +284,31 @@ def test_p8_maximum_principle(orc, omega):
 
 
 # --------------------------------------------------------------------------
+# P10: the paper's own protocol (NEXT-1) obeys the diffusion similarity law.
+# North edge 1, interior 0, omega = 0.376 [P:100], checks every K = 4000
+# iterations, eps = 1e-5 [P:383].  Under-relaxed SOR from a step boundary is
+# a discrete heat equation; its continuum limit is u = erfc(y / 2 sqrt(D k)),
+# whose largest per-iteration change is max_y du/dk = 1 / (sqrt(2 pi e) k)
+# whatever the diffusivity D.  So the checked max-changes must follow
+# 0.24197 / k and the stop test (strict <) first passes at k = 28000 (the
+# first multiple of 4000 above 1/(sqrt(2 pi e) 1e-5) = 24197).  512 x 512 is
+# deep enough that the front (~3 sqrt(D k) ~ 220 rows at k = 28000) stays
+# away from the far ring.
+def test_p10_paper_protocol_similarity_law(orc):
+    c = 1.0 / math.sqrt(2.0 * math.pi * math.e)
+    threads = max(1, min(16, len(os.sched_getaffinity(0))))
+    u = SI.north_hot(512, 512, 1.0)
+    for m in range(1, 8):
+        k = 4000 * m
+        rep = orc.iterate(u, 0.376, 4000, measure_last=True, threads=threads)
+        assert abs(rep.max_change * k / c - 1.0) < 5e-3, (k, rep.max_change)
+    u = SI.north_hot(512, 512, 1.0)
+    rep = orc.solve(u, 0.376, 1e-5, 50000, check_every=4000, threads=threads)
+    assert rep.converged and rep.iters == 28000 and rep.checks == 7
+    assert rep.max_change < 1e-5 and abs(rep.max_change * 28000 / c - 1.0) < 5e-3
+
+
+# --------------------------------------------------------------------------
 # P9 / P15: cadence and accounting
 def test_p9_zero_problem_converges_at_first_check(orc):
     u = np.zeros((10, 12))
