@@ -590,10 +590,15 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
       int64_t r = s.g_lo;
       while (r < s.g_hi) {
         const int64_t i_first = (r - (S - 1)) & ~1LL;
-        // batches needed to finish every remaining row of the strip
+        // batches needed to finish every remaining row of the strip; at least
+        // enough for kMinBand rows (the solve's probe rows recur every 6 rows
+        // from i_first, so a band of >= 6 rows holds one for every stage)
         const int64_t nb_all = (s.g_hi + S - 1 - i_first + 5) / 6;
+        const int64_t kMinBand = 8;
+        const int64_t nb_min = std::min<int64_t>(nb_all, (kMinBand + (S - 1) + (r - i_first) + 5) / 6);
         int64_t nb = std::min<int64_t>(nb_all, (int64_t)Bc);
-        while (nb > 1 && tile_cost(w, r, nb) > Bc) --nb;
+        while (nb > nb_min && tile_cost(w, r, nb) > Bc) --nb;
+        nb = std::max<int64_t>(nb, nb_min);
         const int64_t h = std::max<int64_t>(1, std::min(s.g_hi - r, i_first + 6 * nb - (S - 1) - r));
         if (out_tl) out_tl->push_back(make_int4(w, (int)r, (int)(r + h), 0));
         ++n;
@@ -1008,6 +1013,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     // the max-change cost; after its first inconclusive pass the solve is
     // near the end and switches to all cells (ck=3) to avoid repeated re-runs
     g->every_ck = solve_ck(depth_of(g));
+    int probe_misses = 0;
     while (true) {
       // one segment: iterations k..maxit until the device stops the loop
       CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
@@ -1084,7 +1090,10 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
           if (getenv("SOR_DEBUG"))
             fprintf(stderr, "[sor] re-run at %lld: probe hi %.6e exact %.6e (tol %.3e)\n", (long long)hs.amb_iter,
                     hs.max_change, ex.max_change, tol);
-          if (ex.max_change < sw * tol) g->every_ck = 3;
+          // a probe that keeps missing far from convergence (nothing changes
+          // on its rows yet) would cost a re-run per pass: after the second
+          // inconclusive probe check all cells instead
+          if (ex.max_change < sw * tol || ++probe_misses >= 2) g->every_ck = 3;
         }
         k = pr.k_last + 1;  // g->cur now holds X_{k_last}
         if (k > maxit) {
