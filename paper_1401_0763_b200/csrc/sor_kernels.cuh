@@ -699,14 +699,16 @@ struct WavePipe {
           out[O + 2 * h] = v[h];
           out[1 - O + 2 * h] = C[S - 2][P1][h];
         }
-        if (LANE_OWN && NC % 4 == 0 && sizeof(R) == 8) {
+        if (LANE_OWN && NC % 4 == 0) {
 #pragma unroll
           for (int k = 0; k < NC / 4; ++k)
             stg4_if(inb && ownP[0], orow + 4 * k, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
-        } else if (LANE_OWN && NC % 4 == 0) {
-#pragma unroll
-          for (int k = 0; k < NC / 4; ++k)
-            stg4_if(inb && ownP[0], orow + 4 * k, out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+        } else if (NC == 4) {
+          // ghost band boundaries split a lane (odd T): one 4-wide store for
+          // the fully owned lanes, pair stores only at the two strip edges
+          stg4_if(inb && ownP[0] && ownP[1], orow, out[0], out[1], out[2], out[3]);
+          stg2_if(inb && ownP[0] && !ownP[1], orow, out[0], out[1]);
+          stg2_if(inb && ownP[1] && !ownP[0], orow + 2, out[2], out[3]);
         } else {
 #pragma unroll
           for (int h = 0; h < NH; ++h) stg2_if(inb && ownP[h], orow + 2 * h, out[2 * h], out[2 * h + 1]);
