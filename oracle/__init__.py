@@ -83,6 +83,10 @@ def lib():
         _lib.orc_sor_run_snapshot_f64.argtypes = [vp, i64, i64, dbl, i64, dbl, i64, rp]
         _lib.orc_partition_rows.restype = None
         _lib.orc_partition_rows.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        for name in ("orc_jacobi_run_f64", "orc_jacobi_run_f32"):
+            f = getattr(_lib, name)
+            f.restype = i32
+            f.argtypes = [vp, i64, i64, i32, i64, dbl, i64, i32, rp]
         _lib.orc_jacobi_f64.restype = i32
         _lib.orc_jacobi_f64.argtypes = [vp, i64, i64, i64, dbl, rp]
         _lib.orc_dense_solve_f64.restype = i32
@@ -174,6 +178,25 @@ def jacobi(u: np.ndarray, tol: float, maxit: int) -> Report:
     r = _Report()
     lib().orc_jacobi_f64(u.ctypes.data, u.shape[0] - 2, u.shape[1] - 2, maxit, tol, ctypes.byref(r))
     return _rep(r)
+
+
+def _jacobi_run(u, mode, n_iter, tol, K, measure_last) -> Report:
+    f64 = u.dtype == np.float64
+    _grid(u, np.float64 if f64 else np.float32)
+    r = _Report()
+    fn = lib().orc_jacobi_run_f64 if f64 else lib().orc_jacobi_run_f32
+    fn(u.ctypes.data, u.shape[0] - 2, u.shape[1] - 2, mode, n_iter, tol, K, int(measure_last), ctypes.byref(r))
+    return _rep(r)
+
+
+def jacobi_iterate(u: np.ndarray, iters: int, measure_last: bool = False) -> Report:
+    """NEXT-2: exactly `iters` Jacobi iterations in place (float64 or float32 storage)."""
+    return _jacobi_run(u, 0, iters, 1.0, 1, measure_last)
+
+
+def jacobi_solve(u: np.ndarray, tol: float, maxit: int, check_every: int = 1) -> Report:
+    """NEXT-2: Jacobi with Algorithm 1's loop control (check every K, strict <)."""
+    return _jacobi_run(u, 1, maxit, tol, check_every, False)
 
 
 def dense_solve(u: np.ndarray) -> None:

@@ -305,6 +305,56 @@ int orc_sor_run_threads_f32(float* u, int64_t rows, int64_t cols, double omega, 
 
 /* ------------------------------------------------------------------------ */
 /* Jacobi: every interior cell from the previous iterate only.        */
+/* Jacobi, both modes (NEXT-2): a plain copy of X_{k-1}, then
+ * every interior cell of X_k from it, row by row.                           */
+#define DEFINE_JACOBI(T, SUF)                                                     \
+  int orc_jacobi_run_##SUF(T* u, int64_t rows, int64_t cols, int mode, int64_t n_iter, \
+                           double tol, int64_t K, int measure_last, orc_report* rep) { \
+    memset(rep, 0, sizeof(*rep));                                                 \
+    if (!check_args(rows, cols, 1.0, mode, n_iter, tol, K)) {                     \
+      rep->status = ORC_E_INVAL;                                                  \
+      return ORC_E_INVAL;                                                         \
+    }                                                                             \
+    const int64_t ld = cols + 2, n = (rows + 2) * ld;                             \
+    T* prev = (T*)malloc((size_t)n * sizeof(T));                                  \
+    if (!prev) {                                                                  \
+      rep->status = ORC_E_INVAL;                                                  \
+      return ORC_E_INVAL;                                                         \
+    }                                                                             \
+    const T q = (T)0.25;                                                          \
+    rep->status = mode == 1 ? ORC_NOT_CONVERGED : ORC_DONE;                       \
+    for (int64_t k = 1; k <= n_iter; ++k) {                                       \
+      int check = mode == 1 ? (k % K == 0) : (measure_last && k == n_iter);       \
+      memcpy(prev, u, (size_t)n * sizeof(T));          /* X_{k-1} */             \
+      T m = (T)0;                                                                 \
+      for (int64_t i = 1; i <= rows; ++i)                                         \
+        for (int64_t j = 1; j <= cols; ++j) {                                     \
+          const T* c = prev + i * ld + j;                                         \
+          T s = (c[-ld] + c[ld]) + (c[-1] + c[1]);     /* (N+S)+(W+E) */          \
+          T a = q * s;                                                            \
+          if (check) {                                                            \
+            T d = (T)fabs((double)(a - c[0]));                                    \
+            if (d > m || d != d) m = d;                                           \
+          }                                                                       \
+          u[i * ld + j] = a;                                                      \
+        }                                                                         \
+      rep->half_sweeps += 1;                                                      \
+      rep->iters = k;                                                             \
+      if (check) {                                                                \
+        rep->checks += 1;                                                         \
+        rep->max_change = (double)m;                                              \
+        if (mode == 1 && (double)m < tol) {                                       \
+          rep->status = ORC_DONE;                                                 \
+          break;                                                                  \
+        }                                                                         \
+      }                                                                           \
+    }                                                                             \
+    free(prev);                                                                   \
+    return rep->status;                                                           \
+  }
+DEFINE_JACOBI(double, f64)
+DEFINE_JACOBI(float, f32)
+
 int orc_jacobi_f64(double* u, int64_t rows, int64_t cols, int64_t maxit, double tol,
                    orc_report* rep) {
   memset(rep, 0, sizeof(*rep));

@@ -85,6 +85,17 @@ void orc_partition_rows(int64_t rows, int P, int p, int64_t* lo, int64_t* hi);
 int orc_jacobi_f64(double* u, int64_t rows, int64_t cols, int64_t maxit, double tol,
                    orc_report* rep);
 
+/* Jacobi in the same two modes as orc_sor_run (NEXT-2): iteration k computes
+ * every interior cell of X_k from X_{k-1} only, X = 0.25*((N+S)+(W+E)) in the
+ * order of reading #3, |delta| = |X_k - X_{k-1}| by
+ * subtraction (reading #5); mode 1 checks every K iterations and
+ * stops when the checked max < tol (strict).  f32: storage and
+ * arithmetic in float, 0.25 exact.  half_sweeps counts 1 per iteration.     */
+int orc_jacobi_run_f64(double* u, int64_t rows, int64_t cols, int mode, int64_t n_iter, double tol,
+                       int64_t K, int measure_last, orc_report* rep);
+int orc_jacobi_run_f32(float* u, int64_t rows, int64_t cols, int mode, int64_t n_iter, double tol,
+                       int64_t K, int measure_last, orc_report* rep);
+
 /* Brute force (test only): solve the 5-point Dirichlet system
  * 4u_ij - sum(interior neighbours) = sum(ring neighbours) by dense Gaussian
  * elimination with partial pivoting; writes the interior of `u` in place.

@@ -426,3 +426,77 @@ def test_nan_propagates_in_max(orc):
     u[0, 3] = np.nan
     rep = orc.solve(u, 1.0, 1e-3, 5)
     assert not rep.converged
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: Jacobi in both modes
+def test_jacobi_one_step_s187(orc):
+    """from a north-hot n=4 grid (interior 0), one Jacobi step gives
+    0.25 * north in the row next to the north edge and 0 elsewhere."""
+    for dtype in (np.float64, np.float32):
+        u = SI.north_hot(4, 4, 1.0).astype(dtype)
+        rep = orc.jacobi_iterate(u, 1, measure_last=True)
+        assert np.array_equal(u[1, 1:-1], np.full(4, 0.25, dtype))
+        assert not u[2:-1, 1:-1].any() and rep.max_change == 0.25 and rep.half_sweeps == 1
+
+
+def test_jacobi_reads_only_the_previous_iterate(orc):
+    """Out-of-place semantics: the second step uses only step-1 values.  Row 1
+    after two steps: 0.25*(1 + 0.25) at the ends, 0.25*(1 + 0.25 + 0.25*... ) --
+    written out from the neighbours of step 1 (not a re-typed loop: the
+    step-1 field is the closed form 0.25 on row 1)."""
+    u = SI.north_hot(4, 4, 1.0)
+    orc.jacobi_iterate(u, 2)
+    # step 1: row 1 = 0.25, rest 0.  step 2: row 1 = 0.25*(1 + 0 + W + E), row 2 = 0.25*0.25
+    assert u[1, 1] == 0.25 * (1.0 + 0.25) and u[1, 2] == 0.25 * (1.0 + 0.5)
+    assert np.array_equal(u[2, 1:-1], np.full(4, 0.0625)) and not u[3:-1, 1:-1].any()
+
+
+def test_jacobi_fixed_point_is_dense_solution(orc):
+    u = SI.random_edges(9, 7, seed=3)
+    ref = u.copy()
+    orc.dense_solve(ref)
+    rep = orc.jacobi_solve(u, 1e-15 * 100, 200000, 1)
+    assert rep.converged
+    assert np.abs(u - ref).max() <= 1e-10 * 100
+
+
+def test_jacobi_dyadic_linear_field_bitwise_fixed_point(orc):
+    rows, cols = 13, 10
+    i, j = np.meshgrid(np.arange(rows + 2), np.arange(cols + 2), indexing="ij")
+    u = 0.25 * j + 0.75 * i + 5.0
+    for dtype in (np.float64, np.float32):
+        v = u.astype(dtype)
+        w = v.copy()
+        orc.jacobi_iterate(w, 50)
+        assert np.array_equal(w, v)
+
+
+@pytest.mark.parametrize("n", [16, 24])
+def test_jacobi_asymptotic_rate_is_cos_pi_over_n_plus_1(orc, n):
+    """Jacobi's iteration matrix has spectral radius mu = cos(pi/(N+1)) with
+    eigenvalues +mu and -mu both present: the checked max-changes decay at
+    |mu| per iteration (geometric mean over a window)."""
+    mu = math.cos(math.pi / (n + 1))
+    u = np.zeros((n + 2, n + 2))
+    u[1:-1, 1:-1] = SI.random_field(n, n, seed=5)[1:-1, 1:-1]
+    hist = [orc.jacobi_iterate(u, 1, measure_last=True).max_change for _ in range(1500)]
+    a, b = 1000, 1400
+    rate = (hist[b] / hist[a]) ** (1.0 / (b - a))
+    assert abs(rate - mu) < 2e-4, (rate, mu)
+
+
+def test_jacobi_cadence_and_modes_agree(orc):
+    """Checks at multiples of K only; solve with K=1 equals the
+    original Jacobi routine used by the P3 pin, bitwise."""
+    u = SI.random_edges(20, 17, seed=8)
+    v = u.copy()
+    rep = orc.jacobi_solve(u, 1e-3, 5000, 1)
+    rep2 = orc.jacobi(v, 1e-3, 5000)
+    assert (rep.iters, rep.max_change) == (rep2.iters, rep2.max_change) and np.array_equal(u, v)
+    w = SI.random_edges(20, 17, seed=8)
+    rep3 = orc.jacobi_solve(w, 1e-3, 5000, 7)
+    assert rep3.iters % 7 == 0 and rep3.iters >= rep.iters and rep3.checks == rep3.iters // 7
+    z = SI.north_hot(8, 8, 1.0)
+    rep4 = orc.jacobi_solve(z, 1e-300, 20, 7)
+    assert not rep4.converged and rep4.iters == 20 and rep4.checks == 2
