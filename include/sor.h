@@ -121,6 +121,17 @@ int sor_iterate(sor_grid* g, double omega, int64_t iters, double* last_max_chang
 int sor_solve(sor_grid* g, double omega, double tol, int64_t maxit, int64_t check_every,
               int64_t* iters_out, double* max_change_out);
 
+/* Jacobi (NEXT-2) on the same handle and layout: iteration
+ * k sets every interior cell of X_k to 0.25*((N+S)+(W+E)) of X_{k-1} (the
+ * operation order of reading #3; no relaxation factor).  Same contracts,
+ * outputs and errors as sor_iterate / sor_solve (without omega); the max-
+ * change is |X_k - X_{k-1}| per cell.  Runs on SOR_KERNEL_FUSED (T = 1) and
+ * SOR_KERNEL_TEMPORAL (T Jacobi iterations per HBM pass); other kernels
+ * return SOR_E_UNSUPPORTED.  SOR and Jacobi calls may be mixed on a handle. */
+int sor_jacobi_iterate(sor_grid* g, int64_t iters, double* last_max_change);
+int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
+                     double* max_change_out);
+
 /* Copy the current iterate into `out` ((rows+2)*(cols+2) fp64, host or
  * device; fp32 grids are widened exactly).  Dist: every rank must call; rank
  * 0 receives the whole grid, other ranks' `out` may be NULL.                */

@@ -29,7 +29,7 @@ KERNELS = {"natural": KERNEL_NATURAL, "k1": KERNEL_NATURAL, "fused": KERNEL_FUSE
 EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_id",
            "sor_create_virtual", "sor_set_kernel", "sor_iterate", "sor_solve", "sor_download",
            "sor_download_rows", "sor_reset", "sor_set_stream", "sor_last_elapsed_ms", "sor_get_stats",
-           "sor_partition_rows", "sor_destroy", "sor_last_error")
+           "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve")
 
 
 class SorError(RuntimeError):
@@ -77,6 +77,8 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         "sor_iterate": (i32, [vp, dbl, i64, ctypes.POINTER(dbl)]),
         "sor_solve": (i32, [vp, dbl, dbl, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
         "sor_download": (i32, [vp, vp]),
+        "sor_jacobi_iterate": (i32, [vp, i64, ctypes.POINTER(dbl)]),
+        "sor_jacobi_solve": (i32, [vp, dbl, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
         "sor_download_rows": (i32, [vp, i64, i64, vp]),
         "sor_reset": (i32, [vp, vp]),
         "sor_set_stream": (i32, [vp, vp]),
@@ -204,6 +206,18 @@ class Grid:
         it, m = ctypes.c_int64(0), ctypes.c_double(0.0)
         rc = _check(lib().sor_solve(self._h, omega, tol, maxit, check_every, ctypes.byref(it),
                                     ctypes.byref(m)), allow_not_converged=True)
+        return SolveResult(rc == SOR_OK, it.value, m.value)
+
+    def jacobi(self, iters: int, want_delta: bool = False):
+        """NEXT-2: `iters` Jacobi iterations on the device."""
+        d = ctypes.c_double(0.0)
+        _check(lib().sor_jacobi_iterate(self._h, iters, ctypes.byref(d) if want_delta else None))
+        return d.value if want_delta else None
+
+    def jacobi_solve(self, tol: float, maxit: int, check_every: int = 1) -> SolveResult:
+        it, m = ctypes.c_int64(0), ctypes.c_double(0.0)
+        rc = _check(lib().sor_jacobi_solve(self._h, tol, maxit, check_every, ctypes.byref(it), ctypes.byref(m)),
+                    allow_not_converged=True)
         return SolveResult(rc == SOR_OK, it.value, m.value)
 
     def download(self, out=None):

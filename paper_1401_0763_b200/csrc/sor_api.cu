@@ -93,6 +93,7 @@ struct sor_grid {
   std::map<std::tuple<int, int, int>, std::pair<int4*, int>> tiles;  // (last iteration, (cur after, T))
   int64_t exact_reruns = 0;  // solve passes re-run with exact maxima (diagnostic)
   int every_ck = 4;          // max-change mode of T-deep solve passes with check_every == 1
+  int method = 0;            // 0: red-black SOR; 1: Jacobi (sor_jacobi_*; NEXT-2)
   bool failed = false;
   bool have_elapsed = false;
   double elapsed_ms = 0.0;
@@ -519,17 +520,19 @@ constexpr int wave_nst() { return 14; }
 // resident tiles gives bands <= 512 rows the launch is exactly one wave with
 // batch counts equalised (one_wave below); otherwise ~8 waves of bands >= 256
 // rows in row-major order.
-static bool tile_masked(const sor_grid* g, int T, int wc, int s0, int strip, int64_t R0, int64_t R1) {
-  const int64_t sw = s0 + (int64_t)strip * (wc - 4 * T);
-  const int64_t i_first = (R0 - (2 * T - 1)) & ~1LL;
-  const int64_t nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
+// Geometry: a strip of wc columns overlaps its neighbours by `ghost` columns
+// per side; a pass runs S stages (SOR: ghost = S = 2T; Jacobi: S = T).
+static bool tile_masked(const sor_grid* g, int ghost, int S, int wc, int s0, int strip, int64_t R0, int64_t R1) {
+  const int64_t sw = s0 + (int64_t)strip * (wc - 2 * ghost);
+  const int64_t i_first = (R0 - (S - 1)) & ~1LL;
+  const int64_t nsteps = (R1 + S - 1 - i_first + 5) / 6 * 6;
   return !((sw >= 1) && (sw + wc - 1 <= g->cols) && (i_first - 1 >= 1) &&
            (i_first + nsteps <= g->rows));
 }
 
-int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tiles_per_sm, bool split, int s0,
-               std::pair<int4*, int>* out) {
-  const auto key = std::make_tuple(slab_idx, (T * 2 + (split ? 1 : 0)) * 1024 + wc, tiles_per_sm);
+int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int wc, int tiles_per_sm, bool split,
+               int s0, std::pair<int4*, int>* out) {
+  const auto key = std::make_tuple(slab_idx, ((ghost * 16 + S) * 2 + (split ? 1 : 0)) * 1024 + wc, tiles_per_sm);
   auto it = g->tiles.find(key);
   if (it != g->tiles.end()) {
     *out = it->second;
@@ -549,21 +552,21 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
     e = getenv("SOR_WAVE_MIN_BAND");
     min_h = e ? atoll(e) : 0;
   }
-  const int64_t wout = wc - 4 * T;
-  const int nstrips = (int)((g->cols + 1 - (s0 + 2 * T) + wout - 1) / wout);
+  const int64_t wout = wc - 2 * ghost;
+  const int nstrips = (int)((g->cols + 1 - (s0 + ghost) + wout - 1) / wout);
   const int64_t nrows = s.g_hi - s.g_lo;
   const int64_t slots = (int64_t)g->nsm * tiles_per_sm;
-  const int64_t warm = 4 * T - 2;
+  const int64_t warm = 2 * (S - 1);
   // split strip `w` given the target cost per tile (in row-steps)
   auto split_strip = [&](int w, double cost, std::vector<int4>* tl) {
     int64_t r = s.g_lo;
     while (r < s.g_hi) {
       // try an unmasked-height band first; fall back to the masked height
       int64_t h = std::max<int64_t>(8, (int64_t)(cost - warm));
-      bool m = tile_masked(g, T, wc, s0, w, r, std::min(r + h, s.g_hi));
+      bool m = tile_masked(g, ghost, S, wc, s0, w, r, std::min(r + h, s.g_hi));
       if (m) h = std::max<int64_t>(8, (int64_t)(cost / alpha - warm));
       h = std::min<int64_t>(h, s.g_hi - r);
-      if (tl) tl->push_back(make_int4(w, (int)r, (int)(r + h), tile_masked(g, T, wc, s0, w, r, r + h) ? 1 : 0));
+      if (tl) tl->push_back(make_int4(w, (int)r, (int)(r + h), tile_masked(g, ghost, S, wc, s0, w, r, r + h) ? 1 : 0));
       r += h;
     }
   };
@@ -575,7 +578,6 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
   // others alpha1 on an edge strip (column selects) and 1 elsewhere.  Each
   // tile gets the most batches whose cost fits the budget Bc; Bc is the
   // smallest budget whose tiles fit in one wave.
-  const int S = 2 * T;
   auto tile_cost = [&](int w, int64_t R0, int64_t nb) -> double {
     const int64_t sw = s0 + (int64_t)w * wout;
     const bool col = !(sw >= 1 && sw + wc - 1 <= g->cols);
@@ -610,7 +612,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
   double Bc = 0.0;
   if (waves <= 0) {
     const double kOneWaveMaxB = (512.0 + warm + 5) / 6;
-    for (double b = (double)((4 * T - 2 + 6) / 6 + 1); b <= kOneWaveMaxB; b += 0.125)
+    for (double b = (double)((warm + 6) / 6 + 1); b <= kOneWaveMaxB; b += 0.125)
       if (one_wave(b, nullptr) <= slots) {
         Bc = b;
         break;
@@ -624,7 +626,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int T, int wc, int tile
     double cost;
     if (waves > 0) {
       const int64_t nb = std::max<int64_t>(1, (int64_t)(waves * slots) / nstrips);
-      cost = (double)std::max<int64_t>(min_h > 0 ? min_h : 8 * T, (nrows + nb - 1) / nb) + warm;
+      cost = (double)std::max<int64_t>(min_h > 0 ? min_h : 4 * S, (nrows + nb - 1) / nb) + warm;
     } else {
       const int64_t kMinH = min_h > 0 ? min_h : 256;
       const int64_t nb8 = std::max<int64_t>(1, 8 * slots / nstrips);
@@ -653,8 +655,8 @@ bool wave_pdl(const sor_grid* g) {
 }
 
 // Split mode (a warp pair per tile, stages divided between the two warps) for
-// T >= 2 unless SOR_WAVE_SPLIT=0.
-bool wave_split(int T) {
+// T >= 2 unless SOR_WAVE_SPLIT=0 (with -DSOR_WAVE_NOSPLIT_VARIANTS).
+[[maybe_unused]] bool wave_split(int T) {
   static int sp = -1;
   if (sp < 0) {
     const char* e = getenv("SOR_WAVE_SPLIT");
@@ -687,7 +689,7 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   a.s0 = -4 * ((2 * T + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
   a.tiles = tt.first;
   a.ntiles = tt.second;
   const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta) + (ctl.defer ? 1 : 0);
@@ -715,8 +717,14 @@ template <typename R, int T, int CK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   // 4 columns per lane: wider lanes (NC = 6, 8; bitwise equal) measured
   // slower on B200 at every T (fewer resident warps outweigh the extra ILP)
+  // T >= 2: warp pairs (split); the single-warp variant is built only with
+  // -DSOR_WAVE_NOSPLIT_VARIANTS (SOR_WAVE_SPLIT=0 then selects it)
+#ifdef SOR_WAVE_NOSPLIT_VARIANTS
   if (T >= 2 && wave_split(T)) return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
   return launch_wave_TS<R, T, CK, false, kWaveNC>(g, s, w, ctl, fused_fin);
+#else
+  return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
+#endif
 }
 
 template <typename R, int CK>
@@ -731,6 +739,64 @@ int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
 }
 
+// Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
+template <typename R, int T, int CK>
+int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {
+  constexpr int NST = wave_nst<R>();
+  constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST, kWaveNC>();
+  constexpr int G = jacobi_ghost(T);
+  static int occ = 0;
+  if (occ == 0) {
+    CU(cudaFuncSetAttribute(jacobi_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[g->cur]);
+  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = R(1);
+  a.s0 = -4 * ((G + 3) / 4);
+  const int slab_idx = (int)(&s - &g->slabs[0]);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, slab_idx, G, T, wave_cols<kWaveNC>(), occ * kWaveWarps, false, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  const unsigned blocks = (unsigned)((a.ntiles + kWaveWarps - 1) / kWaveWarps) + (ctl.defer ? 1 : 0);
+  IterCtl c = ctl;
+  c.finalize = fused_fin ? 1 : 0;
+  c.nparts = blocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (wave_pdl(g) && blocks <= (unsigned)(occ * g->nsm)) ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK>, a, c, s.tmap[g->cur]));
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+template <typename R, int CK>
+int launch_jacobi(sor_grid* g, const Slab& s, int T, const IterCtl& ctl, bool fused_fin) {
+  switch (T) {
+    case 1: return launch_jacobi_T<R, 1, CK>(g, s, ctl, fused_fin);
+    case 2: return launch_jacobi_T<R, 2, CK>(g, s, ctl, fused_fin);
+    case 3: return launch_jacobi_T<R, 3, CK>(g, s, ctl, fused_fin);
+    case 4: return launch_jacobi_T<R, 4, CK>(g, s, ctl, fused_fin);
+  }
+  return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
+}
+
 // One HBM pass of ctl.T iterations ending at iteration ctl.k_last.
 template <typename R>
 int wave_pass(sor_grid* g, R w, IterCtl ctl) {
@@ -738,6 +804,15 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   const bool fused_fin = single_part(g) && ctl.ck != 0 && !ctl.defer;
   if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
   for (auto& s : g->slabs) {
+    if (g->method == 1) {  // Jacobi: exact maxima only (ck 1 or 2)
+      if (ctl.ck >= 2)
+        TRY((launch_jacobi<R, 2>(g, s, T, ctl, fused_fin)));
+      else if (ctl.ck == 1)
+        TRY((launch_jacobi<R, 1>(g, s, T, ctl, fused_fin)));
+      else
+        TRY((launch_jacobi<R, 0>(g, s, T, ctl, fused_fin)));
+      continue;
+    }
     if (ctl.ck == 4)
       TRY((launch_wave<R, 4>(g, s, T, w, ctl, fused_fin)));
     else if (ctl.ck == 3)
@@ -1012,7 +1087,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     // far from convergence the probe (ck=4) proves "not converged" at 1/6 of
     // the max-change cost; after its first inconclusive pass the solve is
     // near the end and switches to all cells (ck=3) to avoid repeated re-runs
-    g->every_ck = solve_ck(depth_of(g));
+    g->every_ck = g->method == 1 ? 2 : solve_ck(depth_of(g));
     int probe_misses = 0;
     while (true) {
       // one segment: iterations k..maxit until the device stops the loop
@@ -1241,6 +1316,41 @@ int sor_solve(sor_grid* g, double omega, double tol, int64_t maxit, int64_t chec
     return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
   if (g->dt == SOR_F64) return solve_impl<double>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
   return solve_impl<float>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
+}
+
+namespace {
+struct MethodGuard {  // run one call with the Jacobi method, then restore SOR
+  sor_grid* g;
+  explicit MethodGuard(sor_grid* gg) : g(gg) { g->method = 1; }
+  ~MethodGuard() { g->method = 0; }
+};
+int jacobi_usable(sor_grid* g) {
+  if (g->kernel != SOR_KERNEL_FUSED && g->kernel != SOR_KERNEL_TEMPORAL)
+    return set_error(nullptr, SOR_E_UNSUPPORTED, "Jacobi runs on the FUSED / TEMPORAL kernels only");
+  return SOR_OK;
+}
+}  // namespace
+
+int sor_jacobi_iterate(sor_grid* g, int64_t iters, double* last_max_change) {
+  TRY(usable(g));
+  TRY(jacobi_usable(g));
+  if (iters < 0) return set_error(nullptr, SOR_E_INVAL, "iters must be >= 0");
+  MethodGuard mg(g);
+  if (g->dt == SOR_F64) return iterate_impl<double>(g, 1.0, iters, last_max_change);
+  return iterate_impl<float>(g, 1.0, iters, last_max_change);
+}
+
+int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
+                     double* max_change_out) {
+  TRY(usable(g));
+  TRY(jacobi_usable(g));
+  if (!(tol > 0.0) || !std::isfinite(tol)) return set_error(nullptr, SOR_E_INVAL, "tol must be finite and > 0");
+  if (maxit < 1) return set_error(nullptr, SOR_E_INVAL, "maxit must be >= 1");
+  if (check_every < 1 || check_every > maxit)
+    return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
+  MethodGuard mg(g);
+  if (g->dt == SOR_F64) return solve_impl<double>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
+  return solve_impl<float>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
 }
 
 int sor_download(sor_grid* g, double* out) {

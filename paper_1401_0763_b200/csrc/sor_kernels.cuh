@@ -987,6 +987,249 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
   }
 }
 
+// ---------------------------------------------------------------- Jacobi (NEXT-2)
+// Jacobi [P:95, S:179-187] on the same layout, tiles and TMA source ring as
+// the wave kernel: X_k from X_{k-1} only, X = 0.25*((N+S)+(W+E)).  T
+// iterations per HBM pass = T stages; stage s updates EVERY cell of row i-s
+// from stage s-1's rows r-1, r, r+1 (4 values per lane per row, 3-row rings
+// indexed by step mod 3).  The dependency cone grows one column per stage, so
+// strips overlap by G = T rounded up to even ghost columns per side (even, so
+// stores and ownership stay pair-aligned).  One warp per tile.
+__host__ __device__ constexpr int jacobi_ghost(int T) { return T + (T & 1); }
+
+template <typename R, int T, int NST, int CK>
+struct JacobiPipe {
+  static constexpr int S = T;
+  static constexpr int NC = kWaveNC;
+  static constexpr int WC = wave_cols<NC>();
+  static constexpr int G = jacobi_ghost(T);
+  static constexpr int NSLOT = CK == 2 ? T : 1;
+  static constexpr uint32_t ROWB = WC * sizeof(R);
+  R F[3][NC];                        // source rows, slot = step % 3 phase as in WavePipe
+  R J[S > 1 ? S - 1 : 1][3][NC];     // stage outputs
+  unsigned long long dmax[NSLOT];
+  bool upd[NC];
+  bool ownP[NC / 2];
+  int rows, R0, R1;
+  int col_mask;
+  R* orow;
+  const R* ring;
+  uint32_t ring_s, bar_s;
+  const CUtensorMap* tm;
+  const CUtensorMap* tm2;
+  int tm_x, tm_y;
+  long long pitch;
+  int nbatch;
+  int lane;
+
+  __device__ __forceinline__ void issue_batch_tma(int j) {
+    const uint32_t bar = bar_s + 8u * (j & 1);
+    mbar_expect_tx(bar, 6 * ROWB);
+    tma_rows(ring_s + (j & 1) * 6 * ROWB, tm, tm_x, tm_y + 6 * j + 2, bar);
+  }
+  __device__ __forceinline__ void issue_prologue() {
+    const uint32_t bar = bar_s + 16u;
+    mbar_expect_tx(bar, 2 * ROWB);
+    tma_rows(ring_s + 12 * ROWB, tm2, tm_x, tm_y, bar);
+  }
+  __device__ __forceinline__ void ld_row(const R* row, R (&x)[NC]) { ldsN<NC>(row + NC * lane, x); }
+
+  template <int MK, int M6>
+  __device__ __forceinline__ void step(const WaveArgs<R>& a, int i, const R* rowp) {
+    constexpr int PH = M6 % 3;
+    constexpr int P1 = (PH + 2) % 3;
+    constexpr int P2 = (PH + 1) % 3;
+    ld_row(rowp + M6 * WC, F[P1]);  // source row i+1
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int r = i - s;
+      const int p = s > 0 ? s - 1 : 0;
+      R n[NC], sv[NC], c[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        n[q] = s == 0 ? F[PH][q] : J[p][P2][q];   // row r-1
+        sv[q] = s == 0 ? F[P1][q] : J[p][PH][q];  // row r+1
+        c[q] = s == 0 ? F[P2][q] : J[p][P1][q];   // row r
+      }
+      const R wl = shfl_up1(c[NC - 1]);  // column c0-1 (left lane)
+      const R er = shfl_dn1(c[0]);       // column c0+NC (right lane)
+      R v[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        const R we = radd(q == 0 ? wl : c[q > 0 ? q - 1 : 0], q == NC - 1 ? er : c[q < NC - 1 ? q + 1 : 0]);
+        v[q] = rmul(R(0.25), radd(radd(n[q], sv[q]), we));
+        if (MK == 1) {
+          v[q] = upd[q] ? v[q] : c[q];
+        } else if (MK == 2) {
+          const bool rowok = (unsigned)(r - 1) < (unsigned)rows;
+          v[q] = (rowok && upd[q]) ? v[q] : c[q];
+        }
+      }
+      if (CK == 2 || (CK == 1 && s == S - 1)) {
+        const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
+        const int slot = CK == 2 ? s : 0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+          dmax[slot] = umax64(dmax[slot], (inb && ownP[q >> 1]) ? delta_bits(v[q], c[q]) : 0ull);
+      }
+      if (s < S - 1) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) J[s][PH][q] = v[q];
+      } else {
+        const bool inb = (unsigned)(r - R0) < (unsigned)(R1 - R0);
+        if (G % NC == 0) {
+          stg4_if(inb && ownP[0], orow, v[0], v[1], v[2], v[3]);
+        } else {
+          stg4_if(inb && ownP[0] && ownP[1], orow, v[0], v[1], v[2], v[3]);
+          stg2_if(inb && ownP[0] && !ownP[1], orow, v[0], v[1]);
+          stg2_if(inb && ownP[1] && !ownP[0], orow + 2, v[2], v[3]);
+        }
+        orow += pitch;
+      }
+    }
+  }
+
+  template <int MK>
+  __device__ __forceinline__ void run_range(const WaveArgs<R>& a, int i_first, int j0, int j1) {
+#pragma unroll 1
+    for (int j = j0; j < j1; ++j) {
+      mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
+      const R* rowp = ring + (j & 1) * 6 * WC;
+      const int i = i_first + 6 * j;
+      step<MK, 0>(a, i, rowp);
+      step<MK, 1>(a, i + 1, rowp);
+      step<MK, 2>(a, i + 2, rowp);
+      step<MK, 3>(a, i + 3, rowp);
+      step<MK, 4>(a, i + 4, rowp);
+      step<MK, 5>(a, i + 5, rowp);
+      __syncwarp();
+      if (lane == 0 && j + 2 < nbatch) issue_batch_tma(j + 2);
+    }
+  }
+
+  __device__ __forceinline__ void run(const WaveArgs<R>& a, int i_first) {
+    // rows updated by batch j: i_first+6j-(S-1) .. i_first+6j+5 (see WavePipe::run)
+    const int jA = min(nbatch, max(0, -floordiv6(i_first - S)));
+    const int jB = max(jA, min(nbatch, floordiv6(rows - 5 - i_first) + 1));
+    run_range<2>(a, i_first, 0, jA);
+    if (col_mask)
+      run_range<1>(a, i_first, jA, jB);
+    else
+      run_range<0>(a, i_first, jA, jB);
+    run_range<2>(a, i_first, jB, nbatch);
+  }
+};
+
+template <typename R, int T, int NST, int CK>
+__global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
+    jacobi_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (ctl.st && ctl.solve) {
+    if (ctl.defer && blockIdx.x == 0) {  // the decision block (see wave_kernel)
+      if (threadIdx.x == 0 && ctl.prev_valid && !ld_stop(ctl.st))
+        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set);
+      return;
+    }
+    __shared__ int cta_stop;
+    if (threadIdx.x == 0) cta_stop = ld_stop(ctl.st);
+    __syncthreads();
+    if (cta_stop) return;
+  }
+  extern __shared__ __align__(128) unsigned char wave_smem[];
+  using Pipe = JacobiPipe<R, T, NST, CK>;
+  constexpr int WC = Pipe::WC, NC = Pipe::NC, G = Pipe::G;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = ((int)blockIdx.x - ctl.defer) * kWaveWarps + warp;
+  unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
+  if (gw < a.ntiles) {
+    const int4 tile = a.tiles[gw];
+    const int sw = a.s0 + tile.x * (WC - 2 * G);
+    const int R0 = tile.y, R1 = tile.z;
+    const int i_first = (R0 - (T - 1)) & ~1;
+    const int nsteps = (R1 + T - 1 - i_first + 5) / 6 * 6;
+    unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
+    Pipe P;
+#pragma unroll
+    for (int t = 0; t < Pipe::NSLOT; ++t) P.dmax[t] = 0ull;
+    P.ring = reinterpret_cast<const R*>(wbase);
+    P.ring_s = smem_u32(wbase);
+    P.bar_s = P.ring_s + NST * WC * sizeof(R);
+    P.lane = lane;
+    P.rows = (int)a.rows;
+    P.R0 = R0;
+    P.R1 = R1;
+    const long long c0 = (long long)sw + NC * lane;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int cc = (int)c0 + q;
+      P.upd[q] = (cc >= 1) && (cc <= (int)a.cols);
+    }
+    P.col_mask = (sw >= 1 && sw + WC - 1 <= (int)a.cols) ? 0 : 1;
+    {
+      // ownership by position (see wave_tile): the strip minus G ghost columns per side
+      const int g_lo = sw + G, g_hi = sw + WC - G;
+#pragma unroll
+      for (int h = 0; h < NC / 2; ++h) {
+        const int cp = (int)c0 + 2 * h;
+        P.ownP[h] = cp >= g_lo && cp + 1 < g_hi;
+      }
+    }
+    P.orow = a.dst + (long long)(i_first - (T - 1) - a.g0) * a.pitch + c0;
+#pragma unroll
+    for (int s = 0; s < (T > 1 ? T - 1 : 1); ++s)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) P.J[s][k][q] = R(0);
+    P.pitch = a.pitch;
+    P.tm = &tm.m[0];
+    P.tm2 = &tm.m[1];
+    P.tm_x = kColPad + sw;
+    P.tm_y = i_first - 1 - (int)a.g0;
+    P.nbatch = nsteps / 6;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0) {
+      P.issue_prologue();
+      P.issue_batch_tma(0);
+      if (P.nbatch > 1) P.issue_batch_tma(1);
+    }
+    mbar_wait(P.bar_s + 16u, 0u);
+    P.ld_row(P.ring + 12 * WC, P.F[0]);  // row i_first - 1
+    P.ld_row(P.ring + 13 * WC, P.F[1]);  // row i_first
+    P.run(a, i_first);
+#pragma unroll
+    for (int t = 0; t < Pipe::NSLOT; ++t) dm[t] = P.dmax[t];
+  }
+  if (CK != 0) {
+    constexpr int NS = CK == 2 ? T : 1;
+    __shared__ unsigned long long cta_max[kWaveWarps][NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const unsigned long long m = warp_max_u64(dm[t]);
+      if (lane == 0) cta_max[warp][t] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        unsigned long long m = 0ull;
+#pragma unroll
+        for (int w = 0; w < kWaveWarps; ++w) m = umax64(m, cta_max[w][t]);
+        contribute(ctl, t, m);
+      }
+      maybe_finalize(ctl);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K5
 // Whole grid (rows+2) x (cols+2) in shared memory; Algorithm 1's loop on one
 // CTA.  __syncthreads() is the phase barrier [P:314, P:317].  Used for small
