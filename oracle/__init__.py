@@ -87,6 +87,12 @@ def lib():
             f = getattr(_lib, name)
             f.restype = i32
             f.argtypes = [vp, i64, i64, i32, i64, dbl, i64, i32, rp]
+        for name in ("orc_sor3d_run_f64", "orc_sor3d_run_f32"):
+            f = getattr(_lib, name)
+            f.restype = i32
+            f.argtypes = [vp, i64, i64, i64, dbl, i32, i64, dbl, i64, i32, rp]
+        _lib.orc_dense_solve3d_f64.restype = i32
+        _lib.orc_dense_solve3d_f64.argtypes = [vp, i64, i64, i64]
         _lib.orc_jacobi_f64.restype = i32
         _lib.orc_jacobi_f64.argtypes = [vp, i64, i64, i64, dbl, rp]
         _lib.orc_dense_solve_f64.restype = i32
@@ -197,6 +203,31 @@ def jacobi_iterate(u: np.ndarray, iters: int, measure_last: bool = False) -> Rep
 def jacobi_solve(u: np.ndarray, tol: float, maxit: int, check_every: int = 1) -> Report:
     """NEXT-2: Jacobi with Algorithm 1's loop control (check every K, strict <)."""
     return _jacobi_run(u, 1, maxit, tol, check_every, False)
+
+
+def _sor3d(u, omega, mode, n_iter, tol, K, measure_last) -> Report:
+    f64 = u.dtype == np.float64
+    assert u.ndim == 3 and u.flags.c_contiguous and u.dtype in (np.float64, np.float32)
+    r = _Report()
+    fn = lib().orc_sor3d_run_f64 if f64 else lib().orc_sor3d_run_f32
+    fn(u.ctypes.data, u.shape[0] - 2, u.shape[1] - 2, u.shape[2] - 2, omega, mode, n_iter, tol, K,
+       int(measure_last), ctypes.byref(r))
+    return _rep(r)
+
+
+def sor3d_iterate(u: np.ndarray, omega: float, iters: int, measure_last: bool = False) -> Report:
+    """NEXT-3: 3-D red-black SOR, `iters` iterations in place ((nz+2, ny+2, nx+2) array)."""
+    return _sor3d(u, omega, 0, iters, 1.0, 1, measure_last)
+
+
+def sor3d_solve(u: np.ndarray, omega: float, tol: float, maxit: int, check_every: int = 1) -> Report:
+    return _sor3d(u, omega, 1, maxit, tol, check_every, False)
+
+
+def dense_solve3d(u: np.ndarray) -> None:
+    assert u.ndim == 3 and u.dtype == np.float64 and u.flags.c_contiguous
+    if lib().orc_dense_solve3d_f64(u.ctypes.data, u.shape[0] - 2, u.shape[1] - 2, u.shape[2] - 2) != 0:
+        raise ValueError("dense 3-D solve limited to 1728 unknowns")
 
 
 def dense_solve(u: np.ndarray) -> None:

@@ -355,6 +355,58 @@ int orc_sor_run_threads_f32(float* u, int64_t rows, int64_t cols, double omega, 
 DEFINE_JACOBI(double, f64)
 DEFINE_JACOBI(float, f32)
 
+/* 3-D red-black SOR (NEXT-3): one colour phase, then Algorithm 1's loop.   */
+#define DEFINE_SOR3D(T, SUF, ABS)                                                 \
+  static void phase3d_##SUF(T* u, int64_t nz, int64_t ny, int64_t nx, int c, T w, int check, T* m) { \
+    const int64_t lx = nx + 2, lp = (ny + 2) * lx;                               \
+    const T six = (T)6;                                                          \
+    for (int64_t z = 1; z <= nz; ++z)                                            \
+      for (int64_t y = 1; y <= ny; ++y) {                                        \
+        const int64_t x0 = (((z + y + 1) & 1) == c) ? 1 : 2;  /* (z+y+x)%2 == c */ \
+        for (int64_t x = x0; x <= nx; x += 2) {                                  \
+          T* uc = u + z * lp + y * lx + x;                                       \
+          T s = ((uc[-lx] + uc[lx]) + (uc[-1] + uc[1])) + (uc[-lp] + uc[lp]);   \
+          T a = s / six;                                                         \
+          T r = a - uc[0];                                                       \
+          T un = uc[0] + w * r;                                                  \
+          if (check) {                                                           \
+            T d = ABS(un - uc[0]);                                               \
+            if (d > *m || d != d) *m = d;                                        \
+          }                                                                      \
+          uc[0] = un;                                                            \
+        }                                                                        \
+      }                                                                          \
+  }                                                                              \
+  int orc_sor3d_run_##SUF(T* u, int64_t nz, int64_t ny, int64_t nx, double omega, int mode, \
+                          int64_t n_iter, double tol, int64_t K, int measure_last, orc_report* rep) { \
+    memset(rep, 0, sizeof(*rep));                                                \
+    if (nz < 1 || !check_args(ny, nx, omega, mode, n_iter, tol, K)) {            \
+      rep->status = ORC_E_INVAL;                                                 \
+      return ORC_E_INVAL;                                                        \
+    }                                                                            \
+    const T w = (T)omega;                                                        \
+    rep->status = mode == 1 ? ORC_NOT_CONVERGED : ORC_DONE;                      \
+    for (int64_t k = 1; k <= n_iter; ++k) {                                      \
+      int check = mode == 1 ? (k % K == 0) : (measure_last && k == n_iter);      \
+      T m = (T)0;                                                                \
+      phase3d_##SUF(u, nz, ny, nx, 0, w, check, &m);   /* red */                 \
+      phase3d_##SUF(u, nz, ny, nx, 1, w, check, &m);   /* black */               \
+      rep->half_sweeps += 2;                                                     \
+      rep->iters = k;                                                            \
+      if (check) {                                                               \
+        rep->checks += 1;                                                        \
+        rep->max_change = (double)m;                                             \
+        if (mode == 1 && (double)m < tol) {                                      \
+          rep->status = ORC_DONE;                                                \
+          break;                                                                 \
+        }                                                                        \
+      }                                                                          \
+    }                                                                            \
+    return rep->status;                                                          \
+  }
+DEFINE_SOR3D(double, f64, fabs)
+DEFINE_SOR3D(float, f32, fabsf)
+
 int orc_jacobi_f64(double* u, int64_t rows, int64_t cols, int64_t maxit, double tol,
                    orc_report* rep) {
   memset(rep, 0, sizeof(*rep));
@@ -446,5 +498,58 @@ int orc_dense_solve_f64(double* u, int64_t rows, int64_t cols) {
 #undef IDX
   free(A);
   free(b);
+  return 0;
+}
+
+
+/* 3-D brute force: 6u - sum(interior neighbours) = sum(shell neighbours). */
+int orc_dense_solve3d_f64(double* u, int64_t nz, int64_t ny, int64_t nx) {
+  const int64_t n = nz * ny * nx;
+  if (n > 1728) return -1;
+  const int64_t lx = nx + 2, lp = (ny + 2) * lx;
+  double* A = (double*)calloc((size_t)(n * (n + 1)), sizeof(double));
+  if (!A) return -1;
+#define IDX(z, y, x) (((z) - 1) * ny * nx + ((y) - 1) * nx + ((x) - 1))
+  for (int64_t z = 1; z <= nz; ++z)
+    for (int64_t y = 1; y <= ny; ++y)
+      for (int64_t x = 1; x <= nx; ++x) {
+        const int64_t r = IDX(z, y, x);
+        double* row = A + r * (n + 1);
+        row[r] = 6.0;
+        const int64_t nb[6][3] = {{z, y - 1, x}, {z, y + 1, x}, {z, y, x - 1}, {z, y, x + 1}, {z - 1, y, x}, {z + 1, y, x}};
+        for (int k = 0; k < 6; ++k) {
+          const int64_t zz = nb[k][0], yy = nb[k][1], xx = nb[k][2];
+          if (zz >= 1 && zz <= nz && yy >= 1 && yy <= ny && xx >= 1 && xx <= nx)
+            row[IDX(zz, yy, xx)] -= 1.0;
+          else
+            row[n] += u[zz * lp + yy * lx + xx];
+        }
+      }
+  for (int64_t c = 0; c < n; ++c) {  /* Gaussian elimination, partial pivoting */
+    int64_t p = c;
+    for (int64_t r = c + 1; r < n; ++r)
+      if (fabs(A[r * (n + 1) + c]) > fabs(A[p * (n + 1) + c])) p = r;
+    if (p != c)
+      for (int64_t k = 0; k <= n; ++k) {
+        double t = A[c * (n + 1) + k];
+        A[c * (n + 1) + k] = A[p * (n + 1) + k];
+        A[p * (n + 1) + k] = t;
+      }
+    for (int64_t r = c + 1; r < n; ++r) {
+      const double f = A[r * (n + 1) + c] / A[c * (n + 1) + c];
+      if (f != 0.0)
+        for (int64_t k = c; k <= n; ++k) A[r * (n + 1) + k] -= f * A[c * (n + 1) + k];
+    }
+  }
+  for (int64_t c = n - 1; c >= 0; --c) {
+    double v = A[c * (n + 1) + n];
+    for (int64_t k = c + 1; k < n; ++k) v -= A[c * (n + 1) + k] * A[k * (n + 1) + n];
+    A[c * (n + 1) + n] = v / A[c * (n + 1) + c];
+  }
+  for (int64_t z = 1; z <= nz; ++z)
+    for (int64_t y = 1; y <= ny; ++y)
+      for (int64_t x = 1; x <= nx; ++x) u[z * lp + y * lx + x] = A[IDX(z, y, x) * (n + 1) + n];
+#undef IDX
+  free(A);
   return 0;
 }

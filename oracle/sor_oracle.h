@@ -96,6 +96,22 @@ int orc_jacobi_run_f64(double* u, int64_t rows, int64_t cols, int mode, int64_t 
 int orc_jacobi_run_f32(float* u, int64_t rows, int64_t cols, int mode, int64_t n_iter, double tol,
                        int64_t K, int measure_last, orc_report* rep);
 
+/* 3-D red-black SOR (NEXT-3; the paper's future work): an nz x ny x nx
+ * interior with a Dirichlet shell, storage (nz+2)*(ny+2)*(nx+2) row-major
+ * (z slowest).  Colour of (z, y, x): red iff z+y+x even (reading #11 in 3-D);
+ * red phase first.  Per cell (reading N3-1): s = ((N+S)+(W+E))+(U+D) with
+ * N/S = y-1/y+1, W/E = x-1/x+1, U/D = z-1/z+1; a = s / 6 (correctly rounded
+ * division: the average of the six neighbours); r = a - u; u' = u + w*r.
+ * Modes, cadence and |delta| as orc_sor_run.                                */
+int orc_sor3d_run_f64(double* u, int64_t nz, int64_t ny, int64_t nx, double omega, int mode,
+                      int64_t n_iter, double tol, int64_t K, int measure_last, orc_report* rep);
+int orc_sor3d_run_f32(float* u, int64_t nz, int64_t ny, int64_t nx, double omega, int mode,
+                      int64_t n_iter, double tol, int64_t K, int measure_last, orc_report* rep);
+
+/* Brute force for the 3-D pin (test only): the 7-point Dirichlet system by
+ * dense Gaussian elimination; nz*ny*nx <= 1728.                             */
+int orc_dense_solve3d_f64(double* u, int64_t nz, int64_t ny, int64_t nx);
+
 /* Brute force (test only): solve the 5-point Dirichlet system
  * 4u_ij - sum(interior neighbours) = sum(ring neighbours) by dense Gaussian
  * elimination with partial pivoting; writes the interior of `u` in place.

@@ -134,6 +134,28 @@ class Config:
         return self.rows * self.cols
 
 
+def random_shell3d(nz: int, ny: int, nx: int, seed: int, lo: float = 0.0, hi: float = 100.0) -> np.ndarray:
+    """NEXT-3: (nz+2, ny+2, nx+2) fp64 array; every shell (Dirichlet) cell
+    U[lo, hi) from SplitMix64(seed) in row-major order of the full array
+    (interior draws discarded), interior 0."""
+    u = lo + (hi - lo) * uniform01(seed, (nz + 2) * (ny + 2) * (nx + 2)).reshape(nz + 2, ny + 2, nx + 2)
+    u[1:-1, 1:-1, 1:-1] = 0.0
+    return np.ascontiguousarray(u)
+
+
+def random_field3d(nz: int, ny: int, nx: int, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """NEXT-3: every cell (shell and interior) U[lo, hi) from SplitMix64(seed)."""
+    return np.ascontiguousarray(
+        (lo + (hi - lo) * uniform01(seed, (nz + 2) * (ny + 2) * (nx + 2))).reshape(nz + 2, ny + 2, nx + 2))
+
+
+def top_hot3d(nz: int, ny: int, nx: int, top: float) -> np.ndarray:
+    """NEXT-3: plane z = 0 (the whole face) = top, rest 0."""
+    u = np.zeros((nz + 2, ny + 2, nx + 2))
+    u[0] = top
+    return u
+
+
 def config(name: str, dtype: str | None = None, P: int = 1) -> Config:
     """BASELINE.json configs[0..4] as C1..C5 (+ C5W weak, PAPER = NEXT-1 replay)."""
     if name == "C1":

@@ -500,3 +500,59 @@ def test_jacobi_cadence_and_modes_agree(orc):
     z = SI.north_hot(8, 8, 1.0)
     rep4 = orc.jacobi_solve(z, 1e-300, 20, 7)
     assert not rep4.converged and rep4.iters == 20 and rep4.checks == 2
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: 3-D red-black SOR (7-point, P:410 future work)
+def test_sor3d_fixed_point_is_dense_7point_solution(orc):
+    u = SI.random_shell3d(5, 6, 7, seed=4)
+    ref = u.copy()
+    orc.dense_solve3d(ref)
+    rep = orc.sor3d_solve(u, 1.5, 1e-14 * 100, 100000, 1)
+    assert rep.converged
+    assert np.abs(u - ref).max() <= 1e-11 * 100
+
+
+@pytest.mark.parametrize("omega", [1.0, 1.5])
+def test_sor3d_rate_matches_young(orc, omega):
+    """Red-black ordering of the 7-point Laplacian is consistently ordered: the
+    3-D Jacobi radius on an N^3 cube is mu = cos(pi/(N+1)) and Young's formula
+    gives SOR's rate below omega_opt (P6 in 3-D)."""
+    n = 12
+    mu = math.cos(math.pi / (n + 1))
+    rho = ((omega * mu + math.sqrt(omega * omega * mu * mu - 4 * (omega - 1))) / 2) ** 2
+    u = SI.random_field3d(n, n, n, seed=3)
+    u[0], u[-1], u[:, 0], u[:, -1], u[:, :, 0], u[:, :, -1] = 0, 0, 0, 0, 0, 0
+    hist = [orc.sor3d_iterate(u, omega, 1, measure_last=True).max_change for _ in range(400)]
+    a, b = 300, 390
+    rate = (hist[b] / hist[a]) ** (1.0 / (b - a))
+    assert abs(rate - rho) < 2e-3 * rho, (rate, rho)
+
+
+def test_sor3d_red_first_hand_values(orc):
+    """Top face 1, interior 0, one iteration: red (z+y+x even) first.  Red
+    (1,1,2) sees only the top: omega/6.  Black (1,1,1) then sees the top and
+    the two new red neighbours (1,1,2), (1,2,1): omega*(1 + 2 omega/6)/6.
+    Exact rational values, compared within a few ulps; with the colours
+    swapped both values change at first order."""
+    from fractions import Fraction as F
+    w = 1.5
+    u = SI.top_hot3d(4, 4, 4, 1.0)
+    orc.sor3d_iterate(u, w, 1)
+    red = F(3, 2) / 6
+    black = F(3, 2) * (1 + 2 * red) / 6
+    assert abs(u[1, 1, 2] - float(red)) <= 4e-16 and abs(u[1, 1, 1] - float(black)) <= 4e-16
+    assert u[2, 1, 1] == 0.0 and u[3, 1, 2] == 0.0
+
+
+def test_sor3d_mirror_symmetry_and_f32(orc):
+    u = SI.random_shell3d(6, 5, 9, seed=8)
+    u[:, :, ::-1] = u  # symmetric under x -> nx+1-x (nx odd keeps colours)
+    u = np.ascontiguousarray((u + u[:, :, ::-1]) / 2)
+    orc.sor3d_iterate(u, 1.8, 25)
+    assert np.array_equal(u, u[:, :, ::-1])
+    v = SI.random_shell3d(6, 5, 9, seed=8)
+    w = v.astype(np.float32)
+    orc.sor3d_iterate(v, 1.8, 25)
+    orc.sor3d_iterate(w, 1.8, 25)
+    assert np.abs(w - v).max() <= 1e-5 * 100
