@@ -132,6 +132,24 @@ int sor_jacobi_iterate(sor_grid* g, int64_t iters, double* last_max_change);
 int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
                      double* max_change_out);
 
+/* 3-D red-black SOR (NEXT-3; the paper's future work): a separate
+ * single-GPU handle over an nz x ny x nx interior with a Dirichlet shell.
+ * `init` = caller-owned (nz+2)*(ny+2)*(nx+2) fp64 array, row-major with z
+ * slowest (shell = boundary data, interior = initial guess), host or device,
+ * copied during the call; 1 <= nz, ny <= 65535.  Colour of (z, y, x): red iff
+ * z+y+x even, red phase first; per cell s = ((N+S)+(W+E))+(U+D), a = s/6
+ * (correctly rounded), u' = u + omega*(a - u) (reading N3-1).
+ * iterate / solve / download / errors as the 2-D calls (one kernel form:
+ * in-place colour phases, exact maxima).                                     */
+typedef struct sor3d_grid sor3d_grid;
+int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const double* init, sor_dtype dt);
+int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_change);
+int sor3d_solve(sor3d_grid* g, double omega, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
+                double* max_change_out);
+int sor3d_download(sor3d_grid* g, double* out);
+int sor3d_last_elapsed_ms(const sor3d_grid* g, double* ms);
+void sor3d_destroy(sor3d_grid* g);
+
 /* Copy the current iterate into `out` ((rows+2)*(cols+2) fp64, host or
  * device; fp32 grids are widened exactly).  Dist: every rank must call; rank
  * 0 receives the whole grid, other ranks' `out` may be NULL.                */

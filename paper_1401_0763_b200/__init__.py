@@ -29,7 +29,9 @@ KERNELS = {"natural": KERNEL_NATURAL, "k1": KERNEL_NATURAL, "fused": KERNEL_FUSE
 EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_id",
            "sor_create_virtual", "sor_set_kernel", "sor_iterate", "sor_solve", "sor_download",
            "sor_download_rows", "sor_reset", "sor_set_stream", "sor_last_elapsed_ms", "sor_get_stats",
-           "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve")
+           "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve",
+           "sor3d_create", "sor3d_iterate", "sor3d_solve", "sor3d_download", "sor3d_last_elapsed_ms",
+           "sor3d_destroy")
 
 
 class SorError(RuntimeError):
@@ -86,6 +88,12 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         "sor_get_stats": (i32, [vp, ctypes.POINTER(Stats)]),
         "sor_partition_rows": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "sor_destroy": (None, [vp]),
+        "sor3d_create": (i32, [pp, i64, i64, i64, vp, i32]),
+        "sor3d_iterate": (i32, [vp, dbl, i64, ctypes.POINTER(dbl)]),
+        "sor3d_solve": (i32, [vp, dbl, dbl, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]),
+        "sor3d_download": (i32, [vp, vp]),
+        "sor3d_last_elapsed_ms": (i32, [vp, ctypes.POINTER(dbl)]),
+        "sor3d_destroy": (None, [vp]),
         "sor_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -258,6 +266,66 @@ class Grid:
     def close(self) -> None:
         if self._h is not None and self._h.value:
             lib().sor_destroy(self._h)
+        self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Grid3D:
+    """NEXT-3: a device-resident 3-D red-black SOR grid (sor3d_* handle).
+    Arrays are (nz+2, ny+2, nx+2) C-contiguous fp64 (numpy or torch)."""
+
+    def __init__(self, init, dtype: str = "f64"):
+        if len(tuple(init.shape)) != 3:
+            raise ValueError("init must be 3-D (nz+2, ny+2, nx+2)")
+        self.nz, self.ny, self.nx = (int(d) - 2 for d in init.shape)
+        self.dtype = dtype
+        h = ctypes.c_void_p()
+        if isinstance(init, np.ndarray):
+            if init.dtype != np.float64 or not init.flags.c_contiguous:
+                raise TypeError("grid must be a C-contiguous float64 array")
+            p = init.ctypes.data
+        else:
+            p, _keep = _ptr(init)
+        _check(lib().sor3d_create(ctypes.byref(h), self.nz, self.ny, self.nx, p, F64 if dtype == "f64" else F32))
+        self._h = h
+
+    def iterate(self, omega: float, iters: int, want_delta: bool = False):
+        d = ctypes.c_double(0.0)
+        _check(lib().sor3d_iterate(self._h, omega, iters, ctypes.byref(d) if want_delta else None))
+        return d.value if want_delta else None
+
+    def solve(self, omega: float, tol: float, maxit: int, check_every: int = 1) -> SolveResult:
+        it, m = ctypes.c_int64(0), ctypes.c_double(0.0)
+        rc = _check(lib().sor3d_solve(self._h, omega, tol, maxit, check_every, ctypes.byref(it), ctypes.byref(m)),
+                    allow_not_converged=True)
+        return SolveResult(rc == SOR_OK, it.value, m.value)
+
+    def download(self, out=None):
+        if out is None:
+            out = np.empty((self.nz + 2, self.ny + 2, self.nx + 2), dtype=np.float64)
+        _check(lib().sor3d_download(self._h, out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()))
+        return out
+
+    @property
+    def elapsed_ms(self) -> float:
+        d = ctypes.c_double()
+        _check(lib().sor3d_last_elapsed_ms(self._h, ctypes.byref(d)))
+        return d.value
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            lib().sor3d_destroy(self._h)
         self._h = None
 
     def __enter__(self):

@@ -95,6 +95,8 @@ __device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b); }
 
 // Eq. 1, BJ form, canonical order.  ns = uN+uS and we = uW+uE are formed by the
 // caller (addition is commutative, so which operand is W and which E is moot).
@@ -1225,6 +1227,46 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
         for (int w = 0; w < kWaveWarps; ++w) m = umax64(m, cta_max[w][t]);
         contribute(ctl, t, m);
       }
+      maybe_finalize(ctl);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- 3-D (NEXT-3)
+// 3-D red-black SOR [P:410]: (nz+2) x (ny+2) x (nx+2) grid with a Dirichlet
+// shell; colour of (z, y, x) red iff z+y+x even, red phase first.  Per cell:
+// s = ((N+S)+(W+E))+(U+D) (N/S = y-1/y+1, W/E = x-1/x+1, U/D = z-1/z+1),
+// a = s/6 (correctly rounded division), r = a-u, u' = u + w*r.  One colour
+// phase per launch, in place, one thread per cell of the colour (the K1 form
+// of the 2-D path; 32 algorithmic bytes per update over the two phases).
+// Layout: element (z, y, x) at base + (z*(ny+2) + y)*pitch + x.
+template <typename R, bool CHECK>
+__global__ void __launch_bounds__(256) k3d_half_sweep(R* base, long long pitch, int nz, int ny, int nx, int color,
+                                                      R w, IterCtl ctl) {
+  if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  const int y = blockIdx.y + 1, z = blockIdx.z + 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = ((((z + y + 1) & 1) == color) ? 1 : 2) + 2 * (int)t;
+  const long long plane = (long long)(ny + 2) * pitch;
+  unsigned long long dmax = 0ull;
+  if (x <= nx) {
+    R* uc = base + (long long)z * plane + (long long)y * pitch + x;
+    const R u = uc[0];
+    const R s = radd(radd(radd(uc[-pitch], uc[pitch]), radd(uc[-1], uc[1])), radd(uc[-plane], uc[plane]));
+    const R a = rdiv(s, R(6));
+    const R un = radd(u, rmul(w, rsub(a, u)));
+    if (CHECK) dmax = delta_bits(un, u);
+    uc[0] = un;
+  }
+  if (CHECK) {
+    dmax = warp_max_u64(dmax);
+    __shared__ unsigned long long wmax[8];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0ull;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = umax64(m, wmax[k]);
+      contribute(ctl, 0, m);
       maybe_finalize(ctl);
     }
   }

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "sor.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sor_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sor(?:3d)?_[a-z0-9_]+)\s*\(", src)))
 
 
 def _gpu_present():
