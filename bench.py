@@ -164,6 +164,106 @@ def cpu_baseline(cfg, budget_s: float):
                       f"threaded oracle, {t:.1f} s"}
 
 
+# ------------------------------------------------------------------ NEXT rows
+def run_next(args):
+    """NEXT-2 (Jacobi on C3's grid, 1000 iterations, T-deep passes) and NEXT-3
+    (3-D SOR, 512^3 fp64, 50 iterations, two-pass colour phases): the same
+    JSON contract as the headline line, one GPU."""
+    import torch
+
+    import oracle
+    import paper_1401_0763_b200 as P
+
+    torch.cuda.set_device(0)
+    pk, pk_kind = peaks()
+    if args.method == "jacobi":
+        cfg = SI.config("C3")
+        init_h = cfg.init()
+        iters, units = 1000, cfg.rows * cfg.cols
+        T = args.T
+        g = P.Grid.create(torch.from_numpy(init_h).cuda())
+        g.set_kernel("temporal", T)
+        run = lambda n: g.jacobi(n)                        # noqa: E731
+        reset_d = lambda: g.reset(torch.from_numpy(init_h).cuda())  # noqa: E731
+        bytes_per_update = 16.0 / T
+        kname, workload = f"jacobi_kernel<f64,T={T},ck=0>", f"Jacobi (NEXT-2) on the C3 grid: 4096x4096 f64, {iters} iterations"
+        elapsed = lambda: g.elapsed_ms                     # noqa: E731
+        launches = lambda: g.stats["kernel_launches"]      # noqa: E731
+    else:
+        n = 512
+        init_h = SI.random_shell3d(n, n, n, seed=7)
+        iters, units = 50, n ** 3
+        g = P.Grid3D(init_h)
+        run = lambda k: g.iterate(1.9, k)                  # noqa: E731
+        reset_d = None
+        bytes_per_update = 32.0
+        kname, workload = "k3d_half_sweep<f64> (red + black)", f"3-D red-black SOR (NEXT-3): 512^3 f64, omega 1.9, {iters} iterations"
+        elapsed = lambda: g.elapsed_ms                     # noqa: E731
+        launches = lambda: 2 * iters                       # noqa: E731
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        run(iters)
+        flush.zero_()
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t_dev, n_launch = 0.0, 0
+    for _ in range(args.steps):
+        if reset_d:
+            reset_d()
+        run(iters)
+        t_dev += elapsed()
+        n_launch += launches()
+        flush.zero_()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    value = units * iters * args.steps / (t_dev * 1e-3) / 1e9
+    achieved = value * bytes_per_update
+    line = {
+        "metric": "GLUP/s", "value": value, "unit": "GLUP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_dev / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "method": args.method,
+                   "l2": "flushed between steps (256 MiB write); grids exceed the 126 MB L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": kname,
+                     "algorithmic_bytes_per_update": bytes_per_update, "peak_kind": pk_kind},
+        "gpu_launches": n_launch, "clocks": ck,
+    }
+    # end to end through the C ABI from pinned host buffers
+    hin = torch.from_numpy(init_h).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if args.method == "jacobi":
+            g.reset(hin)
+            g.jacobi(iters)
+            g.download(hout)
+        else:
+            g3 = P.Grid3D(hin.numpy())
+            g3.iterate(1.9, iters)
+            g3.download(hout.numpy())
+            g3.close()
+    t = time.perf_counter() - t0
+    line["e2e"] = {"value": units * iters * args.steps / t / 1e9, "unit": "GLUP/s",
+                   "h2d_bytes_per_step": hin.numel() * 8, "d2h_bytes_per_step": hout.numel() * 8}
+    # the oracle, single thread, bounded sample of the same workload
+    u = init_h.copy()
+    k, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < args.cpu_budget:
+        if args.method == "jacobi":
+            oracle.jacobi_iterate(u, 2)
+        else:
+            oracle.sor3d_iterate(u, 1.9, 1)
+        k += 2 if args.method == "jacobi" else 1
+    tc = time.perf_counter() - t0
+    line["cpu_baseline"] = {"value": units * k / tc / 1e9, "unit": "GLUP/s", "cores": 1, "kind": "oracle",
+                            "sample": f"first {k} iterations of the same grid, single-thread oracle, {tc:.1f} s"}
+    g.close()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -179,11 +279,15 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-iters", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--method", default="sor", choices=["sor", "jacobi", "sor3d"],
+                    help="sor: the headline path; jacobi / sor3d: the NEXT-2 / NEXT-3 rows (1 GPU)")
     args = ap.parse_args()
     if args.dtype is None:
         args.dtype = "f32" if args.config == "C4F32" else "f64"
     if args.impl == "reference":
         return run_reference(args)
+    if args.method != "sor":
+        return run_next(args)
 
     import torch
     import torch.distributed as dist
