@@ -31,7 +31,7 @@ EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_
            "sor_download_rows", "sor_reset", "sor_set_stream", "sor_last_elapsed_ms", "sor_get_stats",
            "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve",
            "sor3d_create", "sor3d_iterate", "sor3d_solve", "sor3d_download", "sor3d_last_elapsed_ms",
-           "sor3d_destroy")
+           "sor3d_destroy", "sor3d_set_kernel")
 
 
 class SorError(RuntimeError):
@@ -94,6 +94,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         "sor3d_download": (i32, [vp, vp]),
         "sor3d_last_elapsed_ms": (i32, [vp, ctypes.POINTER(dbl)]),
         "sor3d_destroy": (None, [vp]),
+        "sor3d_set_kernel": (i32, [vp, i32]),
         "sor_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -299,6 +300,11 @@ class Grid3D:
             p, _keep = _ptr(init)
         _check(lib().sor3d_create(ctypes.byref(h), self.nz, self.ny, self.nx, p, F64 if dtype == "f64" else F32))
         self._h = h
+
+    def set_kernel(self, kernel) -> "Grid3D":
+        k = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+        _check(lib().sor3d_set_kernel(self._h, k))
+        return self
 
     def iterate(self, omega: float, iters: int, want_delta: bool = False):
         d = ctypes.c_double(0.0)

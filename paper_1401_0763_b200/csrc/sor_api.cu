@@ -1462,7 +1462,12 @@ struct sor3d_grid {
   sor_dtype dt = SOR_F64;
   size_t esz = 8;
   int64_t pitch = 0;
-  void* plane = nullptr;
+  void* plane = nullptr;        // the current iterate
+  void* plane2 = nullptr;       // FUSED kernel: the other plane of the ping-pong
+  // default NATURAL: the fused z-wavefront is bitwise equal but slower on
+  // B200 (f64 57 vs 158 GLUP/s at 512^3: the correctly rounded division on its
+  // per-plane critical path, one CTA barrier per plane)
+  int kernel = SOR_KERNEL_NATURAL;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, poll_ev[2] = {nullptr, nullptr};
   DevState* dstate = nullptr;
@@ -1495,6 +1500,7 @@ int set_error3(sor3d_grid* g, int code, const char* fmt, ...) {
 void free3d(sor3d_grid* g) {
   if (!g) return;
   if (g->plane) cudaFree(g->plane);
+  if (g->plane2) cudaFree(g->plane2);
   if (g->dstate) cudaFree(g->dstate);
   if (g->hstate) cudaFreeHost(g->hstate);
   if (g->scratch) cudaFree(g->scratch);
@@ -1519,12 +1525,29 @@ int load3d(sor3d_grid* g, const double* init) {
     narrow_rows<<<grid, 256, 0, g->stream>>>(g->scratch, w, (float*)g->plane, g->pitch, nrow, w);
     CU3(cudaGetLastError());
   }
+  // both planes carry the shell (the fused kernel never writes planes 0, nz+1)
+  CU3(cudaMemcpyAsync(g->plane2, g->plane, bytes, cudaMemcpyDeviceToDevice, g->stream));
   CU3(cudaStreamSynchronize(g->stream));
   return SOR_OK;
 }
 
 template <typename R>
 int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
+  if (g->kernel == SOR_KERNEL_FUSED) {
+    dim3 grid((unsigned)((g->nx + 2 + kX3 - 1) / kX3), (unsigned)((g->ny + 2 + kY3 - 1) / kY3));
+    IterCtl c = ctl;
+    c.finalize = ctl.ck ? 1 : 0;
+    c.nparts = grid.x * grid.y;
+    if (ctl.ck)
+      k3d_fused<R, true><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
+                                                             (int)g->nz, (int)g->ny, (int)g->nx, w, c);
+    else
+      k3d_fused<R, false><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
+                                                              (int)g->nz, (int)g->ny, (int)g->nx, w, c);
+    CU3(cudaGetLastError());
+    std::swap(g->plane, g->plane2);
+    return SOR_OK;
+  }
   const int64_t half = (g->nx + 1) / 2;
   dim3 grid((unsigned)((half + 255) / 256), (unsigned)g->ny, (unsigned)g->nz);
   for (int color = 0; color < 2; ++color) {
@@ -1560,6 +1583,7 @@ int run3d(sor3d_grid* g, double omega, int solve, int64_t n, double tol, int64_t
   const R w = (R)omega;
   const int64_t blk = 64;
   int b = 0;
+  int64_t enq = 0;  // iterations enqueued (launches after a stop exit early)
   for (int64_t k0 = 1; k0 <= n; k0 += blk) {
     const int64_t k1 = std::min(n, k0 + blk - 1);
     for (int64_t k = k0; k <= k1; ++k) {
@@ -1567,6 +1591,7 @@ int run3d(sor3d_grid* g, double omega, int solve, int64_t n, double tol, int64_t
       c.k_last = k;
       c.ck = solve ? (k % K == 0) : (want_last && k == n);
       TRY(k3d_iteration<R>(g, w, c));
+      ++enq;
     }
     if (solve) {
       CU3(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
@@ -1587,6 +1612,10 @@ int run3d(sor3d_grid* g, double omega, int solve, int64_t n, double tol, int64_t
   g->have_elapsed = true;
   const DevState& hs = g->hstate[0];
   *converged = hs.converged != 0;
+  // the fused kernel swapped planes once per enqueued iteration, but those
+  // after the converging one exited without writing
+  if (g->kernel == SOR_KERNEL_FUSED && solve && hs.converged && ((enq - hs.conv_iter) & 1))
+    std::swap(g->plane, g->plane2);
   if (iters_out) *iters_out = solve ? (hs.converged ? hs.conv_iter : n) : n;
   if (max_out) *max_out = (solve || want_last) && n > 0 ? hs.max_change : 0.0;
   return SOR_OK;
@@ -1642,6 +1671,7 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
       break;
     }
     if (cudaMalloc(&g->plane, (size_t)(nz + 2) * (ny + 2) * g->pitch * g->esz) != cudaSuccess ||
+        cudaMalloc(&g->plane2, (size_t)(nz + 2) * (ny + 2) * g->pitch * g->esz) != cudaSuccess ||
         (dt == SOR_F32 && cudaMalloc(&g->scratch, (size_t)n * 8) != cudaSuccess)) {
       cudaGetLastError();
       rc = set_error3(nullptr, SOR_E_NOMEM, "3-D grid allocation failed");
@@ -1695,6 +1725,14 @@ int sor3d_download(sor3d_grid* g, double* out) {
     CU3(cudaMemcpyAsync(out, g->scratch, (size_t)nrow * w * 8, cudaMemcpyDefault, g->stream));
   }
   CU3(cudaStreamSynchronize(g->stream));
+  return SOR_OK;
+}
+
+int sor3d_set_kernel(sor3d_grid* g, int kernel) {
+  if (int rc = usable3(g); rc < 0) return rc;
+  if (kernel != SOR_KERNEL_NATURAL && kernel != SOR_KERNEL_FUSED)
+    return set_error3(nullptr, SOR_E_INVAL, "3-D kernels: SOR_KERNEL_NATURAL or SOR_KERNEL_FUSED");
+  g->kernel = kernel;
   return SOR_OK;
 }
 

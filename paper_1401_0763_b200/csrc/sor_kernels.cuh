@@ -1272,6 +1272,139 @@ __global__ void __launch_bounds__(256) k3d_half_sweep(R* base, long long pitch, 
   }
 }
 
+// Fused 3-D iteration (K3 form): one HBM pass per iteration, src -> dst.  A
+// CTA owns an kX3 x kY3 tile of (y, x) columns and marches down z; each
+// thread holds a PAIR of x-adjacent columns of a (kY3+4) x (kX3+4) window, so
+// in every plane one of its two cells is red and the other black (no
+// divergence between the colour phases).  Step z: the red half-sweep at plane
+// z (the tile plus a 1-column ring, whose new reds the tile's blacks need)
+// from the source, then the black half-sweep at plane z-1 (tile only) from the
+// new reds of planes z-2, z-1, z; plane z-1 of the tile is then final and
+// stored.  In-plane neighbours come from double-buffered shared planes
+// (source plane z, plane z after its red phase); vertical ones from the
+// thread's registers; source planes are loaded kPF steps ahead.  One
+// __syncthreads per step.  Bitwise equal to the two-phase sweep: every cell
+// reads exactly the values the in-place red-then-black order gives it.
+constexpr int kX3 = 64, kY3 = 8;
+constexpr int kW3X = kX3 + 4, kW3Y = kY3 + 4;  // window (columns)
+constexpr int kW3P = kW3X / 2;                 // column pairs per window row
+
+template <typename R, bool CHECK>
+__global__ void __launch_bounds__(kW3P * kW3Y, 3)
+    k3d_fused(const R* __restrict__ src, R* __restrict__ dst, long long pitch, int nz, int ny, int nx, R w,
+              IterCtl ctl) {
+  if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
+  __shared__ R s_src[2][kW3Y][kW3X];  // source plane z (by z parity)
+  __shared__ R s_red[2][kW3Y][kW3X];  // plane z after its red phase (by z parity)
+  const int tp = threadIdx.x % kW3P, ty = threadIdx.x / kW3P;
+  const int tx0 = 2 * tp;  // window column of the pair's first cell
+  const int x0 = blockIdx.x * kX3 - 2 + tx0, y = blockIdx.y * kY3 - 2 + ty;
+  bool inside[2], interior[2], ring1[2], tile[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int x = x0 + e, tx = tx0 + e;
+    inside[e] = x >= 0 && x <= nx + 1 && y >= 0 && y <= ny + 1;
+    interior[e] = x >= 1 && x <= nx && y >= 1 && y <= ny;
+    ring1[e] = tx >= 1 && tx <= kX3 + 2 && ty >= 1 && ty <= kY3 + 2;
+    tile[e] = tx >= 2 && tx < kX3 + 2 && ty >= 2 && ty < kY3 + 2;
+  }
+  const long long plane = (long long)(ny + 2) * pitch;
+  const long long col = (long long)y * pitch + x0;
+  auto ld = [&](int z, int e) -> R {
+    return (inside[e] && z <= nz + 1) ? src[(long long)z * plane + col + e] : R(0);
+  };
+  constexpr int kPF = 4;
+  R q[kPF][2];
+  R sm1[2], s0[2], n2[2], n1[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    sm1[e] = ld(0, e);
+    s0[e] = ld(1, e);
+    n2[e] = n1[e] = sm1[e];  // plane 0 is the shell: fixed
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) q[k][e] = ld(2 + k, e);
+  }
+  unsigned long long dmax = 0ull;
+  auto step = [&](int z, R (&qs)[2]) {
+    R sp1[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      sp1[e] = qs[e];           // plane z+1
+      qs[e] = ld(z + 1 + kPF, e);
+    }
+    const int pz = z & 1;
+    s_src[pz][ty][tx0] = s0[0];
+    s_src[pz][ty][tx0 + 1] = s0[1];
+    __syncthreads();
+    // red phase at plane z: the pair's cell e with (z + y + x0 + e) even
+    // (selects, not indexing: a runtime index would put the pair in local memory)
+    const bool e1 = ((z + y + x0) & 1) != 0;  // the red cell is the pair's second
+    R nz0[2] = {s0[0], s0[1]};
+    {
+      const int tx = tx0 + (e1 ? 1 : 0);
+      const bool upd = e1 ? (ring1[1] && interior[1]) : (ring1[0] && interior[0]);
+      if (z <= nz && upd) {
+        const R sv = e1 ? s0[1] : s0[0];
+        const R s = radd(radd(radd(s_src[pz][ty - 1][tx], s_src[pz][ty + 1][tx]),
+                              radd(s_src[pz][ty][tx - 1], s_src[pz][ty][tx + 1])),
+                         radd(e1 ? sm1[1] : sm1[0], e1 ? sp1[1] : sp1[0]));
+        const R v = radd(sv, rmul(w, rsub(rdiv(s, R(6)), sv)));
+        nz0[0] = e1 ? nz0[0] : v;
+        nz0[1] = e1 ? v : nz0[1];
+        if (CHECK && (e1 ? tile[1] : tile[0])) dmax = umax64(dmax, delta_bits(v, sv));
+      }
+    }
+    s_red[pz][ty][tx0] = nz0[0];
+    s_red[pz][ty][tx0 + 1] = nz0[1];
+    // black phase at plane z-1: the pair's cell with (z-1 + y + x) odd, i.e.
+    // the red index of plane z; its neighbours are reds: in-plane ones of
+    // plane z-1 (shared, previous step), vertical ones of planes z-2, z
+    if (z - 1 >= 1) {
+      const int tx = tx0 + (e1 ? 1 : 0);
+      R out[2] = {n1[0], n1[1]};
+      if (e1 ? (tile[1] && interior[1]) : (tile[0] && interior[0])) {
+        const int qz = pz ^ 1;
+        const R ub = e1 ? n1[1] : n1[0];
+        const R s = radd(radd(radd(s_red[qz][ty - 1][tx], s_red[qz][ty + 1][tx]),
+                              radd(s_red[qz][ty][tx - 1], s_red[qz][ty][tx + 1])),
+                         radd(e1 ? n2[1] : n2[0], e1 ? nz0[1] : nz0[0]));
+        const R v = radd(ub, rmul(w, rsub(rdiv(s, R(6)), ub)));
+        out[0] = e1 ? out[0] : v;
+        out[1] = e1 ? v : out[1];
+        if (CHECK) dmax = umax64(dmax, delta_bits(v, ub));
+      }
+      R* o = dst + (long long)(z - 1) * plane + col;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (tile[e] && inside[e]) o[e] = out[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      n2[e] = n1[e];
+      n1[e] = nz0[e];
+      sm1[e] = s0[e];
+      s0[e] = sp1[e];
+    }
+  };
+  for (int z = 1; z <= nz + 1; z += kPF) {
+#pragma unroll
+    for (int k = 0; k < kPF; ++k)
+      if (z + k <= nz + 1) step(z + k, q[k]);
+  }
+  if (CHECK) {
+    dmax = warp_max_u64(dmax);
+    __shared__ unsigned long long wmax[(kW3P * kW3Y + 31) / 32];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0ull;
+      for (int k = 0; k < (int)((blockDim.x + 31) >> 5); ++k) m = umax64(m, wmax[k]);
+      contribute(ctl, 0, m);
+      maybe_finalize(ctl);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K5
 // Whole grid (rows+2) x (cols+2) in shared memory; Algorithm 1's loop on one
 // CTA.  __syncthreads() is the phase barrier [P:314, P:317].  Used for small

@@ -18,27 +18,31 @@ def gpu(sor):
     return sor
 
 
+@pytest.mark.parametrize("kernel", ["fused", "natural"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_sor3d_iterate_bitwise(gpu, orc, dtype, shape):
+def test_sor3d_iterate_bitwise(gpu, orc, kernel, dtype, shape):
     nz, ny, nx = shape
     init = SI.random_field3d(nz, ny, nx, seed=nz * 100 + ny * 10 + nx, lo=-50.0, hi=100.0)
     ref = init.copy() if dtype == "f64" else init.astype(np.float32)
     rep = orc.sor3d_iterate(ref, 1.7, 9, measure_last=True)
     with gpu.Grid3D(init, dtype=dtype) as g:
+        g.set_kernel(kernel)
         d = g.iterate(1.7, 9, want_delta=True)
         out = g.download()
     assert np.array_equal(out, ref.astype(np.float64))
     assert d == rep.max_change
 
 
+@pytest.mark.parametrize("kernel", ["fused", "natural"])
 @pytest.mark.parametrize("K", [1, 5])
-def test_sor3d_solve_exact(gpu, orc, K):
+def test_sor3d_solve_exact(gpu, orc, kernel, K):
     init = SI.random_shell3d(20, 24, 28, seed=K)
     ref = init.copy()
     rr = orc.sor3d_solve(ref, 1.8, 1e-6, 5000, K)
     rr2 = orc.sor3d_solve(ref, 1.8, 1e-30, 13, 1)
     with gpu.Grid3D(init) as g:
+        g.set_kernel(kernel)
         r = g.solve(1.8, 1e-6, 5000, K)
         r2 = g.solve(1.8, 1e-30, 13, 1)
         out = g.download()
