@@ -908,6 +908,18 @@ __host__ __device__ constexpr int wave_smem_bytes() {
 template <typename R, int T, int NST, int CK, bool SPLIT, int NC>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
     wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
+  const int bid = (int)blockIdx.x - ctl.defer;
+  extern __shared__ __align__(128) unsigned char wave_smem[];
+  constexpr int WC = wave_cols<NC>();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
+  const int role = SPLIT ? warp & 1 : 0;      // 0 front (or whole), 1 back
+  const int gw = bid * wave_tiles_per_cta(SPLIT) + slot;
+  // the tile table is written once by the host: read it before waiting on the
+  // previous launch, so its latency overlaps that wait and the stop read
+  const bool has_tile = bid >= 0 && gw < a.ntiles;
+  const int4 tile = has_tile ? a.tiles[gw] : make_int4(0, 0, 0, 0);
   // Programmatic dependent launch (single slab): the next launch in the
   // stream may be scheduled as soon as every CTA of this one has started;
   // everything this launch reads (source plane, stop flag, maxima) is written
@@ -931,17 +943,8 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     __syncthreads();
     if (cta_stop) return;
   }
-  const int bid = (int)blockIdx.x - ctl.defer;
-  extern __shared__ __align__(128) unsigned char wave_smem[];
-  constexpr int WC = wave_cols<NC>();
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
-  const int role = SPLIT ? warp & 1 : 0;      // 0 front (or whole), 1 back
-  const int gw = bid * wave_tiles_per_cta(SPLIT) + slot;
   unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
-  if (gw < a.ntiles) {
-    const int4 tile = a.tiles[gw];
+  if (has_tile) {
     const int sw = a.s0 + tile.x * (WC - 4 * T);
     const int R0 = tile.y;
     const int R1 = tile.z;
