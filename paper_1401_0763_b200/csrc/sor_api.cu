@@ -1110,7 +1110,12 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     base.defer = (g->kernel != SOR_KERNEL_NATURAL && ensure_third_plane(g)) ? 1 : 0;
     // batches of whole check blocks (and whole passes); poll one batch behind
     const int64_t unit = std::max<int64_t>(K, depth_of(g));
-    const int64_t blk = std::max<int64_t>(unit, (int64_t)((64 + unit - 1) / unit) * unit);
+    static int64_t batch_its = -1;  // iterations enqueued between polls (SOR_SOLVE_BATCH)
+    if (batch_its < 0) {
+      const char* e = getenv("SOR_SOLVE_BATCH");
+      batch_its = e ? std::max<int64_t>(1, atoll(e)) : 64;
+    }
+    const int64_t blk = std::max<int64_t>(unit, (int64_t)((batch_its + unit - 1) / unit) * unit);
     int64_t k = 1;
     int64_t checks = 0;
     // far from convergence the probe (ck=4) proves "not converged" at 1/6 of
