@@ -25,9 +25,10 @@ def test_random_call_sequences(sor, orc, seed):
     for case in range(100):
         rows, cols = rng.randint(1, 300), rng.randint(1, 520)
         kernel, T = rng.choice(KERNELS)
+        dtype = rng.choice(["f64", "f64", "f32"])
         init = SI.random_edges(rows, cols, seed=rng.randint(0, 10**6))
-        ref = init.copy()
-        with sor.Grid.create(init) as g:
+        ref = orc.to_storage(init, dtype)
+        with sor.Grid.create(init, dtype=dtype) as g:
             g.set_kernel(kernel, T)
             for _ in range(rng.randint(1, 5)):
                 op = rng.random()
@@ -38,7 +39,7 @@ def test_random_call_sequences(sor, orc, seed):
                     orc.iterate(ref, omega, k)
                 elif op < 0.4:
                     g.reset(init)
-                    ref = init.copy()
+                    ref = orc.to_storage(init, dtype)
                 else:
                     tol = 10 ** rng.uniform(-9, -2)
                     K = rng.choice([1, 1, 1, 2, 5])
@@ -46,5 +47,5 @@ def test_random_call_sequences(sor, orc, seed):
                     r = g.solve(omega, tol, maxit, K)
                     rr = orc.solve(ref, omega, tol, maxit, K)
                     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
-                        (case, rows, cols, kernel, T)
-            assert np.array_equal(g.download(), ref), (case, rows, cols, kernel, T)
+                        (case, rows, cols, kernel, T, dtype)
+            assert np.array_equal(g.download(), ref.astype(np.float64)), (case, rows, cols, kernel, T, dtype)
