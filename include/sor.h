@@ -176,7 +176,7 @@ int sor_last_elapsed_ms(const sor_grid* g, double* ms);
 
 typedef struct {
   int64_t kernel_launches;  /* library kernels launched by the last iterate/solve call */
-  int64_t half_sweeps;      /* colour phases executed (2 per iteration) */
+  int64_t half_sweeps;      /* colour phases executed (2 per iteration); Jacobi: sweeps */
   int64_t halo_exchanges;   /* halo exchange rounds (dist / virtual)                  */
   int64_t checks;           /* convergence checks evaluated                           */
   int64_t hbm_passes;       /* full read+write passes over the grid                    */

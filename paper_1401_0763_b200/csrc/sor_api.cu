@@ -855,7 +855,7 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   }
   const int src = g->cur;
   g->cur = g->nxt(src);
-  g->st.half_sweeps += 2 * T;
+  g->st.half_sweeps += g->method == 1 ? T : 2 * T;  // Jacobi: one sweep per iteration
   g->st.hbm_passes += 1;
   TRY(exchange(g, g->cur, 2 * T));
   g->halo_valid = 2 * T;
@@ -1234,7 +1234,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
     g->st.checks = checks;
     g->st.exact_reruns = g->exact_reruns;
   }
-  g->st.half_sweeps = 2 * done;
+  g->st.half_sweeps = g->method == 1 ? done : 2 * done;
   if (iters_out) *iters_out = converged ? done : maxit;
   if (max_out) *max_out = maxc;
   return converged ? SOR_OK : SOR_NOT_CONVERGED;

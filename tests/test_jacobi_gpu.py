@@ -47,7 +47,9 @@ def test_jacobi_solve_and_mixing_with_sor(gpu, orc, kernel, T, K):
         g.iterate(1.7, 5)
         r = g.jacobi_solve(1e-3, 3000, K)
         r2 = g.jacobi_solve(1e-30, 30, K)
+        st = g.stats
         out = g.download()
+    assert st["half_sweeps"] == 30          # one Jacobi sweep per iteration
     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
     assert (r2.converged, r2.iters, r2.max_change) == (False, 30, rr2.max_change)
     assert np.array_equal(out, ref)
