@@ -343,7 +343,7 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
   CU(cudaEventCreate(&g->ev1));
   for (int k = 0; k < 2; ++k) CU(cudaEventCreateWithFlags(&g->poll_ev[k], cudaEventDisableTiming));
   CU(cudaMalloc(&g->dstate, sizeof(DevState)));
-  CU(cudaMemset(g->dstate, 0, sizeof(DevState)));
+  CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
   CU(cudaMallocHost(&g->hstate, 2 * sizeof(DevState)));
   memset(g->hstate, 0, 2 * sizeof(DevState));
   CU(cudaMalloc(&g->dflag, sizeof(unsigned int)));
@@ -669,7 +669,11 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int w
                    [](const int4& x, const int4& y) { return x.y != y.y ? x.y < y.y : x.x < y.x; });
   int4* d = nullptr;
   CU(cudaMalloc(&d, tl.size() * sizeof(int4)));
-  CU(cudaMemcpy(d, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  // stream-ordered: a plain cudaMemcpy runs on the legacy stream and, from
+  // pageable memory, may return before the DMA lands, while the kernels run on
+  // a non-blocking stream, so a kernel could read a half-written table (the
+  // suspected cause of one rare fuzz mismatch)
+  CU(cudaMemcpyAsync(d, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice, g->stream));
   *out = {d, (int)tl.size()};
   g->tiles[key] = *out;
   return SOR_OK;
