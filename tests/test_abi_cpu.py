@@ -98,3 +98,13 @@ def test_python_binding_has_no_compute():
     assert "import oracle" not in src and "from oracle" not in src
     for bad in ("0.25", "omega *", "* omega", ".max(", "np.abs("):
         assert bad not in src, bad
+
+
+def test_device_copies_are_stream_ordered():
+    """Every host->device copy and memset in the C-ABI runs on the grid's own
+    (non-blocking) stream: a legacy-stream cudaMemcpy/cudaMemset is not ordered
+    with the kernels and, from pageable memory, may return before the DMA lands."""
+    import re
+    src = open(os.path.join(ROOT, "paper_1401_0763_b200", "csrc", "sor_api.cu")).read()
+    assert not re.findall(r"\bcudaMemcpy(?:2D)?\(", src)
+    assert not re.findall(r"\bcudaMemset\(", src)
