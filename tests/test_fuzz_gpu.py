@@ -49,3 +49,46 @@ def test_random_call_sequences(sor, orc, seed):
                     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
                         (case, rows, cols, kernel, T, dtype)
             assert np.array_equal(g.download(), ref.astype(np.float64)), (case, rows, cols, kernel, T, dtype)
+
+
+@pytest.mark.parametrize("seed", [31])
+def test_random_sor_jacobi_sequences(sor, orc, seed):
+    """SOR and Jacobi (NEXT-2) calls interleaved at random on one handle: the
+    method switch must leave no deferred decision, plane or tile table of one
+    method to the other."""
+    import torch
+    assert torch.cuda.is_available()
+    rng = random.Random(seed)
+    for case in range(80):
+        rows, cols = rng.randint(1, 300), rng.randint(1, 520)
+        kernel, T = rng.choice(KERNELS[:4])          # natural has no Jacobi
+        dtype = rng.choice(["f64", "f64", "f32"])
+        init = SI.random_edges(rows, cols, seed=rng.randint(0, 10**6))
+        ref = orc.to_storage(init, dtype)
+        with sor.Grid.create(init, dtype=dtype) as g:
+            g.set_kernel(kernel, T)
+            for _ in range(rng.randint(2, 6)):
+                op = rng.random()
+                omega = rng.choice([1.0, 1.5, 1.9, 0.376])
+                tol = 10 ** rng.uniform(-8, -2)
+                K = rng.choice([1, 1, 2, 5])
+                maxit = rng.choice([800, 200, 37])
+                if op < 0.2:
+                    k = rng.randint(0, 30)
+                    g.iterate(omega, k)
+                    orc.iterate(ref, omega, k)
+                elif op < 0.4:
+                    k = rng.randint(0, 30)
+                    g.jacobi(k)
+                    orc.jacobi_iterate(ref, k)
+                elif op < 0.7:
+                    r = g.solve(omega, tol, maxit, K)
+                    rr = orc.solve(ref, omega, tol, maxit, K)
+                    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
+                        ("sor", case, rows, cols, kernel, T, dtype)
+                else:
+                    r = g.jacobi_solve(tol, maxit, K)
+                    rr = orc.jacobi_solve(ref, tol, maxit, K)
+                    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
+                        ("jacobi", case, rows, cols, kernel, T, dtype)
+            assert np.array_equal(g.download(), ref.astype(np.float64)), (case, rows, cols, kernel, T, dtype)

@@ -63,3 +63,37 @@ def test_sor3d_errors(gpu):
     bad[2, 2, 2] = np.nan
     with pytest.raises(gpu.SorError):
         gpu.Grid3D(bad)
+
+
+@pytest.mark.parametrize("seed", [41])
+def test_sor3d_random_call_sequences(gpu, orc, seed):
+    """Random iterate / solve sequences on random 3-D shapes, both kernels and
+    dtypes, against the oracle (bitwise): plane swaps after early exits, the
+    stop test at every cadence, continuation across calls."""
+    import random
+    rng = random.Random(seed)
+    for case in range(150):
+        nz, ny, nx = rng.randint(1, 24), rng.randint(1, 30), rng.randint(1, 140)
+        kernel = rng.choice(["fused", "natural"])
+        dtype = rng.choice(["f64", "f64", "f32"])
+        init = SI.random_field3d(nz, ny, nx, seed=rng.randint(0, 10**6), lo=-50.0, hi=100.0)
+        ref = init.copy() if dtype == "f64" else init.astype(np.float32)
+        with gpu.Grid3D(init, dtype=dtype) as g:
+            g.set_kernel(kernel)
+            for _ in range(rng.randint(1, 4)):
+                omega = rng.choice([1.0, 1.5, 1.8, 0.5])
+                if rng.random() < 0.4:
+                    k = rng.randint(0, 25)
+                    g.iterate(omega, k)
+                    orc.sor3d_iterate(ref, omega, k)
+                else:
+                    tol = 10 ** rng.uniform(-8, -1)
+                    K = rng.choice([1, 2, 5])
+                    maxit = rng.choice([500, 60, 7])
+                    if K > maxit:
+                        K = 1
+                    r = g.solve(omega, tol, maxit, K)
+                    rr = orc.sor3d_solve(ref, omega, tol, maxit, K)
+                    assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
+                        (case, nz, ny, nx, kernel, dtype)
+            assert np.array_equal(g.download(), ref.astype(np.float64)), (case, nz, ny, nx, kernel, dtype)
