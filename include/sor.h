@@ -62,6 +62,8 @@ typedef enum {
 
 /* Kernel variants (selected explicitly; there is no auto-dispatch).  All give
  * bitwise-identical results.                                  */
+#define SOR_MAX_T 4  /* deepest temporal blocking (iterations per HBM pass) */
+
 typedef enum {
   SOR_KERNEL_NATURAL = 1,  /* K1: one launch per colour phase, in place, natural layout */
   SOR_KERNEL_FUSED = 3,    /* K3: red+black fused in one HBM pass, src->dst ping-pong  */
@@ -82,26 +84,55 @@ int sor_create_rect(sor_grid** out, int64_t rows, int64_t cols, const double* in
                     sor_dtype dt);
 
 /* Multi-GPU, one process per GPU (row slabs, §8(e)): rank r of nranks owns a
- * contiguous block of interior rows (sizes differ by <= 1),
- * exchanges halo rows with ranks r-1 and r+1 over NCCL (NVLink) and joins the
- * max-change with an NCCL allreduce-max.  `nccl_id` is the 128-byte
- * ncclUniqueId from sor_nccl_unique_id() on rank 0, broadcast by the caller
- * (e.g. torch.distributed).  `device` is the CUDA ordinal for this rank.
- * Every rank passes the full init array.  All later calls on a dist handle
- * are collective: every rank calls them with identical arguments.           */
+ * contiguous block of interior rows (sizes differ by <= 1) — the
+ * P workers of Algorithm 1 each updating their own cells [P:313-317, P:378].
+ * Two transports, the same kernels and bitwise the same results:
+ *
+ * sor_create_dist_ipc (the product path, one node): ranks map each other's
+ *   planes over CUDA IPC; a wave pass's edge tiles store their first/last
+ *   rows straight into the neighbours' halo rows (NVLink peer stores) and
+ *   release a per-strip flag; the edge tiles of the neighbours' next pass
+ *   acquire it, interior tiles never wait, so no global barrier or copy
+ *   separates passes [the paper's per-phase barrier, P:203, P:314-317,
+ *   P:394, becomes neighbour-only flags].  Checked passes join the per-rank
+ *   max-changes through the same mappings (publish / acquire), decided
+ *   speculatively by the next pass's block 0 as on one GPU.  `ipc_id` is the
+ *   128-byte id from sor_ipc_unique_id() on rank 0, broadcast by the caller;
+ *   the ranks meet in a POSIX shared-memory segment of that name (also their
+ *   host barrier for create / reset / download / the start of every call).
+ *   Ranks that share one GPU (a test configuration) run in lockstep: a host
+ *   barrier after every pass, because kernels of different processes on one
+ *   device are time-sliced and must never wait on each other.
+ * sor_create_dist (fallback): halo rows by NCCL send/recv after every pass
+ *   and the max-change by an NCCL allreduce-max; `nccl_id` = the 128-byte
+ *   ncclUniqueId from sor_nccl_unique_id() on rank 0.
+ *
+ * `device` is the CUDA ordinal for this rank.  `init` is read on rank 0
+ * only (the full (rows+2)*(cols+2) array, host or device); other ranks may
+ * pass NULL — rank 0 scatters the slabs (a non-finite init fails every
+ * rank).  Requires rows >= 8*nranks and at most 8 ranks for IPC.  All later
+ * calls on a dist handle are collective: every rank calls them with
+ * identical arguments (a mismatch times out, making the handle failed).     */
 int sor_create_dist(sor_grid** out, int64_t rows, int64_t cols, const double* init,
                     sor_dtype dt, int rank, int nranks, int device, const void* nccl_id);
 int sor_nccl_unique_id(void* out128);
+int sor_create_dist_ipc(sor_grid** out, int64_t rows, int64_t cols, const double* init,
+                        sor_dtype dt, int rank, int nranks, int device, const void* ipc_id);
+int sor_ipc_unique_id(void* out128);
 
 /* Virtual slabs on ONE GPU (test/diagnostic mode): the same slab
- * decomposition, halo layout and kernels as sor_create_dist with `nslabs`
- * slabs, halo rows moved by device-to-device copies instead of NCCL.        */
+ * decomposition, halo layout and kernels as the dist handles with `nslabs`
+ * slabs in one process; halo rows move by the same device-initiated pushes
+ * and flags as sor_create_dist_ipc (SOR_VIRTUAL_COPY=1 in the environment:
+ * by device-to-device copies after every pass instead).                    */
 int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double* init,
                        sor_dtype dt, int nslabs);
 
 /* Select the kernel variant.  temporal_depth T (iterations per HBM pass) is
- * used by SOR_KERNEL_TEMPORAL only, 1 <= T <= 4 (T = 1 equals FUSED).
- * SOR_KERNEL_SMALL requires a single-slab grid that fits in shared memory.
+ * used by SOR_KERNEL_TEMPORAL only, 1 <= T <= SOR_MAX_T (T = 1 equals FUSED;
+ * multi-slab grids need slabs of >= 2T rows).  SOR_KERNEL_SMALL requires a
+ * single-slab grid that fits in shared memory; SOR_KERNEL_NATURAL is not
+ * available on dist-IPC handles (SOR_E_UNSUPPORTED).
  * Returns SOR_E_INVAL / SOR_E_UNSUPPORTED without changing the handle.      */
 int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth);
 
@@ -154,17 +185,18 @@ int sor3d_last_elapsed_ms(const sor3d_grid* g, double* ms);
 void sor3d_destroy(sor3d_grid* g);
 
 /* Copy the current iterate into `out` ((rows+2)*(cols+2) fp64, host or
- * device; fp32 grids are widened exactly).  Dist: every rank must call; rank
- * 0 receives the whole grid, other ranks' `out` may be NULL.                */
+ * device; fp32 grids are widened exactly).  Dist: collective; rank 0
+ * receives the whole grid, other ranks' `out` may be NULL (ignored).       */
 int sor_download(sor_grid* g, double* out);
 
 /* Copy global rows [row_a, row_b) (0 <= row_a < row_b <= rows+2, ring rows
  * included) of the current iterate into `out` ((row_b-row_a)*(cols+2) fp64,
- * host or device).  Single-GPU and virtual handles only.                    */
+ * host or device).  Dist: collective like sor_download (rank 0 receives).   */
 int sor_download_rows(sor_grid* g, int64_t row_a, int64_t row_b, double* out);
 
 /* Re-load the grid from `init` (same contract as sor_create), keeping the
- * handle's allocation, kernel choice and stream.                            */
+ * handle's allocation, kernel choice and stream.  Dist: collective, `init`
+ * read on rank 0 only (NULL allowed elsewhere).                             */
 int sor_reset(sor_grid* g, const double* init);
 
 /* Use an external CUDA stream (cudaStream_t, e.g. torch's current stream) for

@@ -27,6 +27,7 @@ KERNELS = {"natural": KERNEL_NATURAL, "k1": KERNEL_NATURAL, "fused": KERNEL_FUSE
            "temporal": KERNEL_TEMPORAL, "k4": KERNEL_TEMPORAL, "small": KERNEL_SMALL, "k5": KERNEL_SMALL}
 
 EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_id",
+           "sor_create_dist_ipc", "sor_ipc_unique_id",
            "sor_create_virtual", "sor_set_kernel", "sor_iterate", "sor_solve", "sor_download",
            "sor_download_rows", "sor_reset", "sor_set_stream", "sor_last_elapsed_ms", "sor_get_stats",
            "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve",
@@ -74,6 +75,8 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         "sor_create_rect": (i32, [pp, i64, i64, vp, i32]),
         "sor_create_dist": (i32, [pp, i64, i64, vp, i32, i32, i32, i32, vp]),
         "sor_nccl_unique_id": (i32, [vp]),
+        "sor_create_dist_ipc": (i32, [pp, i64, i64, vp, i32, i32, i32, i32, vp]),
+        "sor_ipc_unique_id": (i32, [vp]),
         "sor_create_virtual": (i32, [pp, i64, i64, vp, i32, i32]),
         "sor_set_kernel": (i32, [vp, i32, i32]),
         "sor_iterate": (i32, [vp, dbl, i64, ctypes.POINTER(dbl)]),
@@ -115,20 +118,36 @@ def _check(rc: int, allow_not_converged: bool = False) -> int:
     return rc
 
 
-def _ptr(a, writable: bool = False):
-    """(address, keepalive) of a full fp64 grid buffer (numpy or torch)."""
+def _ptr(a, writable: bool = False, shape=None):
+    """(address, keepalive) of a float64 grid buffer (numpy or torch), after
+    checking dtype, contiguity and (if given) the exact shape the C call will
+    read or write: a wrong size would be an out-of-bounds access in C."""
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or not a.flags.c_contiguous:
             raise TypeError("grid must be a C-contiguous float64 array")
         if writable and not a.flags.writeable:
             raise TypeError("output array is read-only")
+        if shape is not None and tuple(a.shape) != tuple(shape):
+            raise ValueError(f"buffer shape {tuple(a.shape)} != expected {tuple(shape)}")
         return a.ctypes.data, a
     if hasattr(a, "data_ptr"):  # torch.Tensor
         import torch
         if a.dtype != torch.float64 or not a.is_contiguous():
             raise TypeError("grid tensor must be contiguous float64")
+        if shape is not None and tuple(a.shape) != tuple(shape):
+            raise ValueError(f"buffer shape {tuple(a.shape)} != expected {tuple(shape)}")
         return a.data_ptr(), a
     raise TypeError(f"unsupported grid buffer {type(a)!r}")
+
+
+_DTYPES = {"f64": F64, "f32": F32}
+
+
+def _dt(dtype: str) -> int:
+    try:
+        return _DTYPES[dtype]
+    except KeyError:
+        raise ValueError(f"dtype must be 'f64' or 'f32', got {dtype!r}") from None
 
 
 def partition_rows(rows: int, P: int, p: int) -> tuple[int, int]:
@@ -140,6 +159,13 @@ def partition_rows(rows: int, P: int, p: int) -> tuple[int, int]:
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().sor_nccl_unique_id(buf))
+    return buf.raw
+
+
+def ipc_unique_id() -> bytes:
+    """Rendezvous id of a dist-IPC handle (rank 0 makes it; broadcast it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().sor_ipc_unique_id(buf))
     return buf.raw
 
 
@@ -162,29 +188,45 @@ class Grid:
     def create(cls, init, dtype: str = "f64", rows: int | None = None, cols: int | None = None):
         rows, cols = cls._dims(init, rows, cols)
         h = ctypes.c_void_p()
-        p, _keep = _ptr(init)
-        _check(lib().sor_create_rect(ctypes.byref(h), rows, cols, p, F64 if dtype == "f64" else F32))
+        p, _keep = _ptr(init, shape=(rows + 2, cols + 2))
+        _check(lib().sor_create_rect(ctypes.byref(h), rows, cols, p, _dt(dtype)))
         return cls(h.value, rows, cols, dtype)
 
     @classmethod
     def create_virtual(cls, init, nslabs: int, dtype: str = "f64"):
         rows, cols = cls._dims(init, None, None)
         h = ctypes.c_void_p()
-        p, _keep = _ptr(init)
-        _check(lib().sor_create_virtual(ctypes.byref(h), rows, cols, p, F64 if dtype == "f64" else F32,
-                                        nslabs))
+        p, _keep = _ptr(init, shape=(rows + 2, cols + 2))
+        _check(lib().sor_create_virtual(ctypes.byref(h), rows, cols, p, _dt(dtype), nslabs))
         return cls(h.value, rows, cols, dtype)
 
     @classmethod
-    def create_dist(cls, init, rank: int, nranks: int, device: int, nccl_id: bytes,
-                    dtype: str = "f64"):
-        rows, cols = cls._dims(init, None, None)
+    def _create_dist(cls, fn, init, rank, nranks, device, uid, dtype, rows, cols):
+        if init is None:
+            if rows is None or cols is None:
+                raise ValueError("init=None needs rows and cols")
+            p, _keep = None, None
+        else:
+            rows, cols = cls._dims(init, rows, cols)
+            p, _keep = _ptr(init, shape=(rows + 2, cols + 2))
         h = ctypes.c_void_p()
-        p, _keep = _ptr(init)
-        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
-        _check(lib().sor_create_dist(ctypes.byref(h), rows, cols, p, F64 if dtype == "f64" else F32,
-                                     rank, nranks, device, idbuf))
-        return cls(h.value, rows, cols, dtype)
+        idbuf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(fn(ctypes.byref(h), rows, cols, p, _dt(dtype), rank, nranks, device, idbuf))
+        g = cls(h.value, rows, cols, dtype)
+        g.rank, g.nranks = rank, nranks
+        return g
+
+    @classmethod
+    def create_dist(cls, init, rank: int, nranks: int, device: int, nccl_id: bytes,
+                    dtype: str = "f64", rows: int | None = None, cols: int | None = None):
+        """Dist handle over NCCL (fallback transport); init only on rank 0."""
+        return cls._create_dist(lib().sor_create_dist, init, rank, nranks, device, nccl_id, dtype, rows, cols)
+
+    @classmethod
+    def create_dist_ipc(cls, init, rank: int, nranks: int, device: int, ipc_id: bytes,
+                        dtype: str = "f64", rows: int | None = None, cols: int | None = None):
+        """Dist handle over CUDA IPC (device-initiated halo push); init only on rank 0."""
+        return cls._create_dist(lib().sor_create_dist_ipc, init, rank, nranks, device, ipc_id, dtype, rows, cols)
 
     @staticmethod
     def _dims(init, rows, cols):
@@ -229,10 +271,17 @@ class Grid:
                     allow_not_converged=True)
         return SolveResult(rc == SOR_OK, it.value, m.value)
 
+    def _receives(self) -> bool:
+        return getattr(self, "rank", 0) == 0
+
     def download(self, out=None):
+        """The whole grid; dist handles: collective, rank 0 receives (others get None)."""
+        if not self._receives():
+            _check(lib().sor_download(self._h, None))
+            return None
         if out is None:
             out = np.empty((self.rows + 2, self.cols + 2), dtype=np.float64)
-        p, _keep = _ptr(out, writable=True) if out is not False else (None, None)
+        p, _keep = _ptr(out, writable=True, shape=(self.rows + 2, self.cols + 2))
         _check(lib().sor_download(self._h, p))
         return out
 
@@ -241,15 +290,23 @@ class Grid:
         _check(lib().sor_download(self._h, None))
 
     def download_rows(self, row_a: int, row_b: int, out=None):
-        """Global rows [row_a, row_b) (ring rows count: 0 is the north ring)."""
+        """Global rows [row_a, row_b) (ring rows count: 0 is the north ring).
+        Dist handles: collective, rank 0 receives (others get None)."""
+        if not self._receives():
+            _check(lib().sor_download_rows(self._h, row_a, row_b, None))
+            return None
         if out is None:
-            out = np.empty((row_b - row_a, self.cols + 2), dtype=np.float64)
-        p, _keep = _ptr(out, writable=True)
+            out = np.empty((max(0, row_b - row_a), self.cols + 2), dtype=np.float64)
+        p, _keep = _ptr(out, writable=True, shape=(max(0, row_b - row_a), self.cols + 2))
         _check(lib().sor_download_rows(self._h, row_a, row_b, p))
         return out
 
     def reset(self, init) -> None:
-        p, _keep = _ptr(init)
+        """Reload from init (dist: collective; init read on rank 0, None elsewhere)."""
+        if init is None:
+            _check(lib().sor_reset(self._h, None))
+            return
+        p, _keep = _ptr(init, shape=(self.rows + 2, self.cols + 2))
         _check(lib().sor_reset(self._h, p))
 
     @property
@@ -292,13 +349,8 @@ class Grid3D:
         self.nz, self.ny, self.nx = (int(d) - 2 for d in init.shape)
         self.dtype = dtype
         h = ctypes.c_void_p()
-        if isinstance(init, np.ndarray):
-            if init.dtype != np.float64 or not init.flags.c_contiguous:
-                raise TypeError("grid must be a C-contiguous float64 array")
-            p = init.ctypes.data
-        else:
-            p, _keep = _ptr(init)
-        _check(lib().sor3d_create(ctypes.byref(h), self.nz, self.ny, self.nx, p, F64 if dtype == "f64" else F32))
+        p, _keep = _ptr(init)
+        _check(lib().sor3d_create(ctypes.byref(h), self.nz, self.ny, self.nx, p, _dt(dtype)))
         self._h = h
 
     def set_kernel(self, kernel) -> "Grid3D":
@@ -318,9 +370,11 @@ class Grid3D:
         return SolveResult(rc == SOR_OK, it.value, m.value)
 
     def download(self, out=None):
+        shape = (self.nz + 2, self.ny + 2, self.nx + 2)
         if out is None:
-            out = np.empty((self.nz + 2, self.ny + 2, self.nx + 2), dtype=np.float64)
-        _check(lib().sor3d_download(self._h, out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()))
+            out = np.empty(shape, dtype=np.float64)
+        p, _keep = _ptr(out, writable=True, shape=shape)
+        _check(lib().sor3d_download(self._h, p))
         return out
 
     @property

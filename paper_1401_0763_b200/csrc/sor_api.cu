@@ -27,81 +27,27 @@
 #include <thread>
 #include <vector>
 
-#include "sor.h"
-#include "sor_kernels.cuh"
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
-using namespace sorb;
+#include <atomic>
+#include <chrono>
+#include <random>
 
-namespace {
+#include "sor_internal.h"
 
+static_assert(SOR_MAX_T == sorb::kMaxT, "include/sor.h and the kernels disagree on the deepest T");
+
+namespace sorh {
 thread_local std::string g_last_error;
+}  // namespace sorh
 
-struct Slab {
-  int64_t g_lo = 0, g_hi = 0;  // owned global interior rows [g_lo, g_hi)
-  int64_t g0 = 0;              // global row of storage row 0 (= g_lo - kRowPad)
-  int64_t nstore = 0;          // storage rows
-  // planes 0, 1: ping-pong; plane 2 (allocated on the first deferred solve):
-  // the speculative pass of the deferred stop test writes the third plane
-  void* plane[3] = {nullptr, nullptr, nullptr};
-  WaveMaps tmap[3];  // per plane: tensor maps of the wave kernel's source-row boxes
-};
+using namespace sorh;
 
-enum class Mode { Single, Virtual, Dist };
-
-struct KernelCache {
-  int occ_blocks = 0;  // resident CTAs per SM for the wave kernel instance
-};
-
-}  // namespace
-
-struct sor_grid {
-  int64_t rows = 0, cols = 0;
-  sor_dtype dt = SOR_F64;
-  size_t esz = 8;
-  int64_t pitch = 0;  // elements
-  Mode mode = Mode::Single;
-  std::vector<Slab> slabs;
-  int cur = 0;  // plane holding the current iterate (same for all slabs)
-  int kernel = SOR_KERNEL_FUSED;
-  int tdepth = 1;
-  int device = 0;
-  int nsm = 148;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
-  DevState* dstate = nullptr;
-  DevState* hstate = nullptr;  // pinned, 2 slots for one-batch-behind polling
-  double* scratch = nullptr;   // f64 staging for f32 pack/unpack and dist gather
-  size_t scratch_bytes = 0;
-  unsigned int* dflag = nullptr;
-  int rank = 0, nranks = 1;
-  ncclComm_t comm = nullptr;
-  int halo_valid = kRowPad;  // rows of the current plane's halos known up to date
-  struct PassRec {
-    int64_t k_last;
-    int src, dst, T;
-  };
-  std::vector<PassRec> pass_ends;  // wave passes of the current solve segment
-  int nplanes = 2;                 // planes in rotation (3 once the deferred solve allocated plane 2)
-  int nxt(int p) const { return (p + 1) % nplanes; }
-  // deferred stop test: the last checked pass not yet decided, and the slot set
-  // the next checked pass contributes to
-  bool prev_valid = false;
-  int prev_T = 0, prev_ck = 0, prev_set = 0, next_set = 0;
-  int64_t prev_k_last = 0;
-  // wave-kernel tile tables per (slab, T, occupancy): device int4 array + count
-  std::map<std::tuple<int, int, int>, std::pair<int4*, int>> tiles;  // (last iteration, (cur after, T))
-  int64_t exact_reruns = 0;  // solve passes re-run with exact maxima (diagnostic)
-  int every_ck = 4;          // max-change mode of T-deep solve passes with check_every == 1
-  int method = 0;            // 0: red-black SOR; 1: Jacobi (sor_jacobi_*; NEXT-2)
-  bool failed = false;
-  bool have_elapsed = false;
-  double elapsed_ms = 0.0;
-  sor_stats st{};
-};
-
-namespace {
+namespace sorh {
 
 int set_error(sor_grid* g, int code, const char* fmt, ...) {
   char buf[512];
@@ -113,28 +59,6 @@ int set_error(sor_grid* g, int code, const char* fmt, ...) {
   if (g && (code == SOR_E_CUDA || code == SOR_E_NCCL)) g->failed = true;
   return code;
 }
-
-#define CU(call)                                                                      \
-  do {                                                                                \
-    cudaError_t e_ = (call);                                                          \
-    if (e_ != cudaSuccess)                                                            \
-      return set_error(g, SOR_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
-  } while (0)
-
-#define NC(call)                                                                      \
-  do {                                                                                \
-    ncclResult_t r_ = (call);                                                         \
-    if (r_ != ncclSuccess)                                                            \
-      return set_error(g, SOR_E_NCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
-  } while (0)
-
-#define TRY(expr)             \
-  do {                        \
-    int rc_ = (expr);         \
-    if (rc_ < 0) return rc_;  \
-  } while (0)
-
-int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at{};
@@ -154,12 +78,164 @@ int partition(int64_t rows, int P, int p, int64_t* lo, int64_t* hi) {
   return SOR_OK;
 }
 
-template <typename R>
-R* col0(void* plane) {
-  return reinterpret_cast<R*>(plane) + kColPad;
-}
 
 cudaMemcpyKind kDefault = cudaMemcpyDefault;
+
+// ------------------------------------------------------------------ dist-IPC rendezvous
+// The ranks of a dist-IPC handle are processes on one node.  They meet in a
+// POSIX shared-memory segment named by the 128-byte id (sor_ipc_unique_id on
+// rank 0, broadcast by the caller), publish their CUDA-IPC handles there and
+// use it as a host barrier for the collective calls (create, reset,
+// download, the start of iterate/solve, exact re-runs, and every pass in
+// lockstep mode).  Kernels synchronise through device flags (HaloLink,
+// DistComm), never through this segment.
+struct RankInfo {
+  cudaIpcMemHandle_t plane[3];
+  cudaIpcMemHandle_t comm;
+  int64_t g_lo, g_hi, g0, nstore;
+  char bus_id[32];
+  int nplanes;
+  int ok;
+  unsigned long long seq;
+};
+struct ShmHdr {
+  uint32_t magic;
+  uint32_t nranks;
+  std::atomic<uint32_t> arrived;
+  std::atomic<uint32_t> generation;
+  std::atomic<int32_t> status;  // rank 0's verdict on the init (scatter), shared with all
+  RankInfo rank[kMaxRanks];
+};
+static_assert(std::atomic<uint32_t>::is_always_lock_free, "process-shared atomics need lock-free types");
+constexpr uint32_t kShmMagic = 0x534f5242u;  // "SORB"
+
+struct ShmSeg {
+  ShmHdr* h = nullptr;
+  std::string name;
+  bool owner = false;
+};
+
+int shm_open_seg(sor_grid* g, const char* id, int rank, int nranks) {
+  char name[128];
+  memcpy(name, id, 127);
+  name[127] = 0;
+  if (name[0] != '/' || strlen(name) < 8) return set_error(nullptr, SOR_E_INVAL, "dist-ipc: bad id (use sor_ipc_unique_id)");
+  ShmSeg* s = new ShmSeg();
+  s->name = name;
+  int fd = -1;
+  if (rank == 0) {
+    fd = shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) {
+      delete s;
+      return set_error(nullptr, SOR_E_STATE, "dist-ipc: shm_open(%s) failed (id reused?)", name);
+    }
+    if (ftruncate(fd, sizeof(ShmHdr)) != 0) {
+      close(fd);
+      shm_unlink(name);
+      delete s;
+      return set_error(nullptr, SOR_E_STATE, "dist-ipc: ftruncate failed");
+    }
+    s->owner = true;
+  } else {
+    const auto t0 = std::chrono::steady_clock::now();
+    while ((fd = shm_open(name, O_RDWR, 0600)) < 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+        delete s;
+        return set_error(nullptr, SOR_E_STATE, "dist-ipc: rank %d: segment %s never appeared", rank, name);
+      }
+      usleep(1000);
+    }
+    struct stat stt{};
+    while (fstat(fd, &stt) == 0 && (size_t)stt.st_size < sizeof(ShmHdr)) usleep(1000);
+  }
+  void* p = mmap(nullptr, sizeof(ShmHdr), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    if (rank == 0) shm_unlink(name);
+    delete s;
+    return set_error(nullptr, SOR_E_STATE, "dist-ipc: mmap failed");
+  }
+  s->h = reinterpret_cast<ShmHdr*>(p);
+  if (rank == 0) {
+    s->h->nranks = (uint32_t)nranks;
+    s->h->arrived.store(0);
+    s->h->generation.store(0);
+    s->h->status.store(0);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    __atomic_store_n(&s->h->magic, kShmMagic, __ATOMIC_RELEASE);
+  } else {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (__atomic_load_n(&s->h->magic, __ATOMIC_ACQUIRE) != kShmMagic) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+        munmap(p, sizeof(ShmHdr));
+        delete s;
+        return set_error(nullptr, SOR_E_STATE, "dist-ipc: segment never initialised");
+      }
+      usleep(500);
+    }
+    if (s->h->nranks != (uint32_t)nranks) {
+      munmap(p, sizeof(ShmHdr));
+      delete s;
+      return set_error(nullptr, SOR_E_INVAL, "dist-ipc: nranks mismatch between ranks");
+    }
+  }
+  g->shm = s;
+  return SOR_OK;
+}
+
+void shm_close_seg(ShmSeg* s) {
+  if (!s) return;
+  if (s->h) munmap(s->h, sizeof(ShmHdr));
+  if (s->owner) shm_unlink(s->name.c_str());
+  delete s;
+}
+
+// Host barrier of all ranks (sense by generation).  Spins with yields; gives
+// up after `timeout_s` (a rank that died or diverged must not hang the rest).
+int shm_barrier(sor_grid* g, double timeout_s = 300.0) {
+  ShmHdr* h = g->shm->h;
+  const uint32_t gen = h->generation.load(std::memory_order_acquire);
+  if (h->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == h->nranks) {
+    h->arrived.store(0, std::memory_order_relaxed);
+    h->generation.fetch_add(1, std::memory_order_acq_rel);
+    return SOR_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (h->generation.load(std::memory_order_acquire) == gen) {
+    if (++spins > 256) {
+      sched_yield();
+      if ((spins & 1023) == 0 &&
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+      {
+        g->failed = true;  // the ranks disagree on the call sequence; nothing can recover
+        return set_error(g, SOR_E_STATE, "dist-ipc: barrier timed out on rank %d", g->rank);
+      }
+    }
+  }
+  return SOR_OK;
+}
+
+// Barrier of a dist-IPC handle; a no-op for every other handle.
+int dist_barrier(sor_grid* g) {
+  if (g->transport != Transport::Ipc) return SOR_OK;
+  return shm_barrier(g);
+}
+
+// Dist-IPC: every rank takes the largest pass sequence number of all ranks
+// (passes enqueued after a stop exit early without releasing any flag, so
+// any common value at least as large as every released one is consistent).
+int sync_seq(sor_grid* g) {
+  if (g->transport != Transport::Ipc) return SOR_OK;
+  ShmHdr* h = g->shm->h;
+  h->rank[g->rank].seq = g->seq;
+  TRY(shm_barrier(g));
+  unsigned long long m = 0;
+  for (int q = 0; q < g->nranks; ++q) m = std::max<unsigned long long>(m, h->rank[q].seq);
+  TRY(shm_barrier(g));
+  g->seq = m;
+  return SOR_OK;
+}
 
 // ------------------------------------------------------------------ layout
 // Copy global rows [ga, gb) of a full (rows+2)x(cols+2) fp64 array into plane p
@@ -266,6 +342,10 @@ int check_finite(sor_grid* g, const double* init, int64_t n, bool on_device) {
     }
     return SOR_OK;
   }
+  // a device-resident init may still be being written by the caller's work on
+  // another stream (torch's current stream, the legacy stream): order every
+  // read of it after all of that work
+  CU(cudaDeviceSynchronize());
   CU(cudaMemsetAsync(g->dflag, 0, sizeof(unsigned int), g->stream));
   count_nonfinite<<<4 * g->nsm, 256, 0, g->stream>>>(init, n, g->dflag);
   CU(cudaGetLastError());
@@ -276,20 +356,28 @@ int check_finite(sor_grid* g, const double* init, int64_t n, bool on_device) {
   return SOR_OK;
 }
 
-// Fill both planes of every slab from init: global rows within the slab's
-// storage window that exist in [0, rows+1] (own rows, ring, initial halos).
-int load_all(sor_grid* g, const double* init) {
-  for (auto& s : g->slabs) {
-    const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
-    CU(cudaMemsetAsync(s.plane[0], 0, bytes, g->stream));
-    const int64_t ga = std::max<int64_t>(0, s.g0);
-    const int64_t gb = std::min<int64_t>(g->rows + 2, s.g0 + s.nstore);
-    TRY(load_rows(g, s, 0, init, ga, gb));
-    for (int p = 1; p < 3; ++p)
-      if (s.plane[p]) CU(cudaMemcpyAsync(s.plane[p], s.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
-  }
+void reset_plane_info(sor_grid* g) {
+  for (auto& pi : g->pinfo) pi = PlaneInfo{};
   g->cur = 0;
   g->halo_valid = kRowPad;
+}
+
+// Fill every plane of slab s from init: global rows within the slab's storage
+// window that exist in [0, rows+1] (own rows, ring, initial halos).
+int load_slab(sor_grid* g, const Slab& s, const double* init) {
+  const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
+  CU(cudaMemsetAsync(s.plane[0], 0, bytes, g->stream));
+  const int64_t ga = std::max<int64_t>(0, s.g0);
+  const int64_t gb = std::min<int64_t>(g->rows + 2, s.g0 + s.nstore);
+  TRY(load_rows(g, s, 0, init, ga, gb));
+  for (int p = 1; p < 3; ++p)
+    if (s.plane[p]) CU(cudaMemcpyAsync(s.plane[p], s.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
+  return SOR_OK;
+}
+
+int load_all(sor_grid* g, const double* init) {
+  for (auto& s : g->slabs) TRY(load_slab(g, s, init));
+  reset_plane_info(g);
   CU(cudaStreamSynchronize(g->stream));
   return SOR_OK;
 }
@@ -305,6 +393,8 @@ int validate_dims(int64_t rows, int64_t cols) {
 
 void free_grid(sor_grid* g) {
   if (!g) return;
+  if (g->device >= 0) cudaSetDevice(g->device);
+  for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto& s : g->slabs)
     for (int p = 0; p < 3; ++p)
       if (s.plane[p]) cudaFree(s.plane[p]);
@@ -312,6 +402,8 @@ void free_grid(sor_grid* g) {
   if (g->hstate) cudaFreeHost(g->hstate);
   if (g->scratch) cudaFree(g->scratch);
   if (g->dflag) cudaFree(g->dflag);
+  if (g->flagbuf) cudaFree(g->flagbuf);
+  if (g->djoin) cudaFree(g->djoin);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   for (int k = 0; k < 2; ++k)
@@ -319,12 +411,12 @@ void free_grid(sor_grid* g) {
   if (g->own_stream) cudaStreamDestroy(g->own_stream);
   if (g->comm) ncclCommDestroy(g->comm);
   for (auto& kv : g->tiles) cudaFree(kv.second.first);
+  shm_close_seg(g->shm);
   delete g;
 }
 
-// Common construction.  slabs_lo_hi: owned row ranges of the slabs this
-// handle holds.
-int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, int64_t>>& spans) {
+// Device buffers, streams and the slabs' planes (zeroed; not loaded).
+int build(sor_grid* g, const std::vector<std::pair<int64_t, int64_t>>& spans, int nplanes) {
   int dev = 0;
   CU(cudaGetDevice(&dev));
   g->device = dev;
@@ -358,21 +450,53 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
     s.g_hi = sp.second;
     s.g0 = s.g_lo - kRowPad;
     s.nstore = (s.g_hi - s.g_lo) + 2 * kRowPad;
-    for (int p = 0; p < 2; ++p) {
-      cudaError_t e = cudaMalloc(&s.plane[p], (size_t)s.nstore * g->pitch * g->esz);
+    const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
+    for (int p = 0; p < nplanes; ++p) {
+      cudaError_t e = cudaMalloc(&s.plane[p], bytes);
       if (e != cudaSuccess) {
         cudaGetLastError();
         g->slabs.push_back(s);
-        return set_error(nullptr, SOR_E_NOMEM, "cudaMalloc of %.3f GB plane failed: %s",
-                         (double)s.nstore * g->pitch * g->esz / 1e9, cudaGetErrorString(e));
+        return set_error(nullptr, SOR_E_NOMEM, "cudaMalloc of %.3f GB plane failed: %s", (double)bytes / 1e9,
+                         cudaGetErrorString(e));
       }
+      CU(cudaMemsetAsync(s.plane[p], 0, bytes, g->stream));
     }
     g->slabs.push_back(s);
-    for (int p = 0; p < 2; ++p) TRY(make_tmaps(g, g->slabs.back(), p));
+    for (int p = 0; p < nplanes; ++p) TRY(make_tmaps(g, g->slabs.back(), p));
   }
-  const bool on_dev = is_device_ptr(init);
-  TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
-  TRY(load_all(g, init));
+  g->nplanes = nplanes;
+  // halo flags: per slab a top and a bottom array of nflags (one per strip of
+  // any layout); dist-IPC puts them behind this rank's DistComm header
+  g->nflags = (int)(g->cols / 64 + 8);
+  if (g->push) {
+    const size_t fl = (size_t)2 * g->nflags * sizeof(unsigned long long);
+    const size_t hdr = g->mode == Mode::Dist ? sizeof(DistComm) : 0;
+    const size_t bytes = hdr + fl * g->slabs.size();
+    CU(cudaMalloc(&g->flagbuf, bytes));
+    CU(cudaMemsetAsync(g->flagbuf, 0, bytes, g->stream));
+    for (size_t k = 0; k < g->slabs.size(); ++k) {
+      auto* f = reinterpret_cast<unsigned long long*>((char*)g->flagbuf + hdr + fl * k);
+      g->slabs[k].ftop = f;
+      g->slabs[k].fbot = f + g->nflags;
+    }
+    g->H = 2 * kMaxT;
+  }
+  if (g->mode == Mode::Virtual) {  // neighbours are the adjacent slabs
+    const int n = (int)g->slabs.size();
+    for (int k = 0; k < n; ++k) {
+      for (int d = 0; d < 2; ++d) {
+        const int q = d == 0 ? k - 1 : k + 1;
+        if (q < 0 || q >= n) continue;
+        Neighbour& nb = d == 0 ? g->slabs[k].up : g->slabs[k].dn;
+        nb.ok = true;
+        for (int p = 0; p < 3; ++p) nb.plane[p] = g->slabs[q].plane[p];
+        nb.ftop = g->slabs[q].ftop;
+        nb.fbot = g->slabs[q].fbot;
+        nb.g0 = g->slabs[q].g0;
+      }
+    }
+  }
+  CU(cudaStreamSynchronize(g->stream));
   g->st.nslabs = (int32_t)g->slabs.size();
   g->st.rank = g->rank;
   g->st.nranks = g->nranks;
@@ -384,11 +508,188 @@ int build(sor_grid* g, const double* init, const std::vector<std::pair<int64_t, 
   return SOR_OK;
 }
 
-int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
-                  Mode mode, int nslabs, int rank, int nranks, int device, const void* nccl_id) {
+// ---- dist over NCCL: rank 0 scatters the init (fp64 rows) to every rank
+int scatter_nccl(sor_grid* g, const double* init) {
+  const int64_t w = g->cols + 2;
+  const Slab& me = g->slabs[0];
+  int32_t* dstat = reinterpret_cast<int32_t*>(g->dflag);
+  // rank 0's verdict on the init first, so a bad init fails every rank
+  if (g->rank == 0) {
+    const bool on_dev = is_device_ptr(init);
+    const int rc = check_finite(g, init, (g->rows + 2) * w, on_dev);
+    const int32_t st = rc < 0 ? 1 : 0;
+    CU(cudaMemcpyAsync(dstat, &st, sizeof st, cudaMemcpyHostToDevice, g->stream));
+  }
+  NC(ncclBroadcast(dstat, dstat, 1, ncclInt32, 0, g->comm, g->stream));
+  int32_t st = 0;
+  CU(cudaMemcpyAsync(&st, dstat, sizeof st, cudaMemcpyDeviceToHost, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  if (st) return set_error(nullptr, SOR_E_INVAL, "init (rank 0) contains non-finite values");
+  if (g->rank == 0) TRY(load_slab(g, me, init));
+  // a staging buffer of whole rows for the transfers
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)((64 << 20) / (w * 8)));
+  double* xbuf = nullptr;
+  CU(cudaMalloc(&xbuf, (size_t)chunk * w * 8));
+  int rc = SOR_OK;
+  for (int p = 1; p < g->nranks && rc == SOR_OK; ++p) {
+    int64_t lo, hi;
+    partition(g->rows, g->nranks, p, &lo, &hi);
+    const int64_t ga = std::max<int64_t>(0, lo - kRowPad), gb = std::min<int64_t>(g->rows + 2, hi + kRowPad);
+    if (g->rank != 0 && g->rank != p) continue;
+    for (int64_t r = ga; r < gb && rc == SOR_OK; r += chunk) {
+      const int64_t n = std::min(chunk, gb - r);
+      ncclResult_t nr;
+      if (g->rank == 0) {
+        if (cudaMemcpyAsync(xbuf, init + r * w, n * w * 8, kDefault, g->stream) != cudaSuccess) {
+          rc = set_error(g, SOR_E_CUDA, "scatter: copy failed");
+          break;
+        }
+        nr = ncclSend(xbuf, n * w, ncclFloat64, p, g->comm, g->stream);
+      } else {
+        nr = ncclRecv(xbuf, n * w, ncclFloat64, 0, g->comm, g->stream);
+      }
+      if (nr != ncclSuccess) {
+        rc = set_error(g, SOR_E_NCCL, "scatter: %s", ncclGetErrorString(nr));
+        break;
+      }
+      if (g->rank == p) {
+        if (r == ga) {
+          if (cudaMemsetAsync(me.plane[0], 0, (size_t)me.nstore * g->pitch * g->esz, g->stream) != cudaSuccess) {
+            rc = set_error(g, SOR_E_CUDA, "scatter: memset failed");
+            break;
+          }
+        }
+        rc = load_rows(g, me, 0, xbuf - r * w, r, r + n);
+      }
+      if (cudaStreamSynchronize(g->stream) != cudaSuccess) rc = set_error(g, SOR_E_CUDA, "scatter: sync failed");
+    }
+  }
+  cudaFree(xbuf);
+  TRY(rc);
+  if (g->rank != 0) {
+    const size_t bytes = (size_t)me.nstore * g->pitch * g->esz;
+    for (int p = 1; p < 3; ++p)
+      if (me.plane[p]) CU(cudaMemcpyAsync(me.plane[p], me.plane[0], bytes, cudaMemcpyDeviceToDevice, g->stream));
+  }
+  reset_plane_info(g);
+  CU(cudaStreamSynchronize(g->stream));
+  return SOR_OK;
+}
+
+// ---- dist over CUDA IPC: publish, map, scatter
+int ipc_open(sor_grid* g, const cudaIpcMemHandle_t& h, void** out) {
+  CU(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  g->ipc_opened.push_back(*out);
+  return SOR_OK;
+}
+
+int ipc_connect(sor_grid* g, const char* id) {
+  TRY(shm_open_seg(g, id, g->rank, g->nranks));
+  ShmHdr* H = g->shm->h;
+  Slab& s = g->slabs[0];
+  RankInfo& me = H->rank[g->rank];
+  for (int p = 0; p < 3; ++p) CU(cudaIpcGetMemHandle(&me.plane[p], s.plane[p]));
+  CU(cudaIpcGetMemHandle(&me.comm, g->flagbuf));
+  me.g_lo = s.g_lo;
+  me.g_hi = s.g_hi;
+  me.g0 = s.g0;
+  me.nstore = s.nstore;
+  me.nplanes = 3;
+  CU(cudaDeviceGetPCIBusId(me.bus_id, sizeof me.bus_id, g->device));
+  me.ok = 1;
+  TRY(shm_barrier(g));
+  // ranks sharing a GPU run in lockstep: kernels of different processes on
+  // one device are time-sliced, never co-resident, so none may wait on another
+  bool share = getenv("SOR_DIST_LOCKSTEP") != nullptr;
+  for (int q = 0; q < g->nranks; ++q)
+    for (int r = q + 1; r < g->nranks; ++r)
+      if (strncmp(H->rank[q].bus_id, H->rank[r].bus_id, sizeof me.bus_id) == 0) share = true;
+  g->lockstep = share;
+  DistJoinTab tab{};
+  tab.nranks = g->nranks;
+  tab.rank = g->rank;
+  const size_t fl_off = sizeof(DistComm);
+  if (g->rank == 0) g->rslabs.resize(g->nranks);
+  for (int q = 0; q < g->nranks; ++q) {
+    const RankInfo& ri = H->rank[q];
+    void* comm = nullptr;
+    void* pl[3] = {nullptr, nullptr, nullptr};
+    if (q == g->rank) {
+      comm = g->flagbuf;
+      for (int p = 0; p < 3; ++p) pl[p] = s.plane[p];
+    } else {
+      TRY(ipc_open(g, ri.comm, &comm));
+      if (q == g->rank - 1 || q == g->rank + 1 || g->rank == 0)
+        for (int p = 0; p < 3; ++p) TRY(ipc_open(g, ri.plane[p], &pl[p]));
+    }
+    tab.comm[q] = reinterpret_cast<DistComm*>(comm);
+    auto* f = reinterpret_cast<unsigned long long*>((char*)comm + fl_off);
+    if (q == g->rank - 1 || q == g->rank + 1) {
+      Neighbour& nb = q < g->rank ? s.up : s.dn;
+      nb.ok = true;
+      for (int p = 0; p < 3; ++p) nb.plane[p] = pl[p];
+      nb.ftop = f;
+      nb.fbot = f + g->nflags;
+      nb.g0 = ri.g0;
+    }
+    if (g->rank == 0) {
+      Slab& rs = g->rslabs[q];
+      rs.g_lo = ri.g_lo;
+      rs.g_hi = ri.g_hi;
+      rs.g0 = ri.g0;
+      rs.nstore = ri.nstore;
+      for (int p = 0; p < 3; ++p) rs.plane[p] = pl[p];
+    }
+  }
+  CU(cudaMalloc(&g->djoin, sizeof(DistJoinTab)));
+  CU(cudaMemcpyAsync(g->djoin, &tab, sizeof tab, cudaMemcpyHostToDevice, g->stream));
+  CU(cudaStreamSynchronize(g->stream));
+  return shm_barrier(g);
+}
+
+// Rank 0 writes every rank's planes through the IPC mappings; the barrier
+// after it publishes them.  A bad init fails every rank (shared status).
+int scatter_ipc(sor_grid* g, const double* init) {
+  ShmHdr* H = g->shm->h;
+  if (g->rank == 0) {
+    const bool on_dev = is_device_ptr(init);
+    int rc = check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev);
+    if (rc == SOR_OK) {
+      for (int q = 0; q < g->nranks && rc == SOR_OK; ++q) rc = load_slab(g, g->rslabs[q], init);
+      if (rc == SOR_OK && cudaStreamSynchronize(g->stream) != cudaSuccess)
+        rc = set_error(g, SOR_E_CUDA, "scatter: sync failed");
+    }
+    H->status.store(rc, std::memory_order_release);
+    TRY(shm_barrier(g));
+    TRY(rc);
+  } else {
+    TRY(shm_barrier(g));
+    const int rc = H->status.load(std::memory_order_acquire);
+    if (rc < 0) return set_error(nullptr, rc, "init rejected on rank 0: %s", rc == SOR_E_INVAL ? "non-finite values" : "error");
+  }
+  reset_plane_info(g);
+  TRY(shm_barrier(g));  // status read by all before it can change again
+  return SOR_OK;
+}
+
+// (Re)load a handle from `init` (dist: collective; rank 0's init).
+int load_grid(sor_grid* g, const double* init) {
+  if (g->mode != Mode::Dist) {
+    if (!init) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
+    const bool on_dev = is_device_ptr(init);
+    TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
+    return load_all(g, init);
+  }
+  if (g->rank == 0 && !init) return set_error(nullptr, SOR_E_INVAL, "init is NULL on rank 0");
+  if (g->transport == Transport::Ipc) return scatter_ipc(g, init);
+  return scatter_nccl(g, init);
+}
+
+int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt, Mode mode,
+                  int nslabs, int rank, int nranks, int device, const void* id, Transport tr) {
   if (!out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
   *out = nullptr;
-  if (!init) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
+  if (!init && (mode != Mode::Dist || rank == 0)) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
   if (dt != SOR_F64 && dt != SOR_F32) return set_error(nullptr, SOR_E_INVAL, "bad dtype %d", (int)dt);
   TRY(validate_dims(rows, cols));
   std::vector<std::pair<int64_t, int64_t>> spans;
@@ -405,14 +706,12 @@ int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init
   } else {
     if (nranks < 1 || rank < 0 || rank >= nranks || rows < 8LL * nranks)
       return set_error(nullptr, SOR_E_INVAL, "dist: need 0 <= rank < nranks and rows >= 8*nranks");
-    if (!nccl_id) return set_error(nullptr, SOR_E_INVAL, "dist: nccl_id is NULL");
+    if (tr == Transport::Ipc && nranks > kMaxRanks)
+      return set_error(nullptr, SOR_E_INVAL, "dist-ipc: at most %d ranks (one node)", kMaxRanks);
+    if (!id) return set_error(nullptr, SOR_E_INVAL, "dist: id is NULL");
     int64_t lo, hi;
     partition(rows, nranks, rank, &lo, &hi);
     spans.push_back({lo, hi});
-  }
-  if (mode == Mode::Dist) {
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) return set_error(nullptr, SOR_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
   }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -421,6 +720,10 @@ int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init
     return set_error(nullptr, SOR_E_CUDA, "no CUDA device available (%s); libsor has no CPU fallback",
                      cudaGetErrorString(e));
   }
+  if (mode == Mode::Dist) {
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return set_error(nullptr, SOR_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
   sor_grid* g = new sor_grid();
   g->rows = rows;
   g->cols = cols;
@@ -428,17 +731,18 @@ int create_common(sor_grid** out, int64_t rows, int64_t cols, const double* init
   g->mode = mode;
   g->rank = mode == Mode::Dist ? rank : 0;
   g->nranks = mode == Mode::Dist ? nranks : 1;
-  if (mode == Mode::Dist) {
-    ncclUniqueId id;
-    memcpy(&id, nccl_id, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&g->comm, nranks, id, rank);
-    if (r != ncclSuccess) {
-      set_error(nullptr, SOR_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
-      free_grid(g);
-      return SOR_E_NCCL;
-    }
+  g->transport = mode == Mode::Dist ? tr : Transport::None;
+  g->push = (mode == Mode::Virtual && !getenv("SOR_VIRTUAL_COPY")) || g->transport == Transport::Ipc;
+  int rc = SOR_OK;
+  if (g->transport == Transport::Nccl) {
+    ncclUniqueId nid;
+    memcpy(&nid, id, sizeof nid);
+    ncclResult_t r = ncclCommInitRank(&g->comm, nranks, nid, rank);
+    if (r != ncclSuccess) rc = set_error(nullptr, SOR_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
-  int rc = build(g, init, spans);
+  if (rc == SOR_OK) rc = build(g, spans, g->transport == Transport::Ipc ? 3 : 2);
+  if (rc == SOR_OK && g->transport == Transport::Ipc) rc = ipc_connect(g, reinterpret_cast<const char*>(id));
+  if (rc == SOR_OK) rc = load_grid(g, init);
   if (rc < 0) {
     free_grid(g);
     return rc;
@@ -454,8 +758,11 @@ int usable(sor_grid* g) {
 }
 
 // ------------------------------------------------------------------ halos
-// After a pass wrote plane p: each slab sends its first/last h owned rows to
-// the neighbouring slabs' halo rows of the same plane.
+// Host-side halo exchange (virtual copies, NCCL send/recv, or IPC copies in
+// lockstep): after a pass wrote plane p, each slab sends its first/last h
+// owned rows to the neighbouring slabs' halo rows of the same plane.  The
+// push modes (virtual, dist-IPC) use it only when a pass needs more halo
+// rows than the last push delivered (K1 passes, a deeper T after set_kernel).
 int exchange(sor_grid* g, int p, int h) {
   const size_t row_bytes = (size_t)g->pitch * g->esz;
   if (g->mode == Mode::Virtual) {
@@ -472,11 +779,28 @@ int exchange(sor_grid* g, int p, int h) {
                          h * row_bytes, cudaMemcpyDeviceToDevice, g->stream));
     }
     g->st.halo_exchanges += 1;
+    g->pinfo[p].wseq = 0;
     return SOR_OK;
   }
   if (g->mode != Mode::Dist || g->nranks == 1) return SOR_OK;
   Slab& s = g->slabs[0];
   char* pl = (char*)s.plane[p];
+  if (g->transport == Transport::Ipc) {
+    // every rank's pass is complete before, and every copy after (barriers)
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));
+    if (s.up.ok)
+      CU(cudaMemcpyAsync((char*)s.up.plane[p] + (s.g_lo - s.up.g0) * row_bytes, pl + (s.g_lo - s.g0) * row_bytes,
+                         h * row_bytes, cudaMemcpyDeviceToDevice, g->stream));
+    if (s.dn.ok)
+      CU(cudaMemcpyAsync((char*)s.dn.plane[p] + (s.g_hi - h - s.dn.g0) * row_bytes,
+                         pl + (s.g_hi - h - s.g0) * row_bytes, h * row_bytes, cudaMemcpyDeviceToDevice, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));
+    g->st.halo_exchanges += 1;
+    g->pinfo[p].wseq = 0;
+    return SOR_OK;
+  }
   const ncclDataType_t ty = ncclUint8;
   const size_t n = h * row_bytes;
   NC(ncclGroupStart());
@@ -490,21 +814,82 @@ int exchange(sor_grid* g, int p, int h) {
   }
   NC(ncclGroupEnd());
   g->st.halo_exchanges += 1;
+  g->pinfo[p].wseq = 0;
   return SOR_OK;
+}
+
+// Cross-rank join mode of the maxima (IterCtl::join_mode).
+int join_mode_of(const sor_grid* g) {
+  if (g->transport != Transport::Ipc || g->nranks == 1) return 0;
+  return g->lockstep ? 2 : 1;
 }
 
 // Join the per-slab maxima and run the stop test (multi-slab modes).
 int join_and_finalize(sor_grid* g, const IterCtl& ctl) {
-  if (g->mode == Mode::Dist && g->nranks > 1)
-    NC(ncclAllReduce(&g->dstate->maxbits[0][0], &g->dstate->maxbits[0][0], kMaxT * 16, ncclUint64, ncclMax,
+  if (g->transport == Transport::Nccl && g->nranks > 1)
+    NC(ncclAllReduce(&g->dstate->maxbits[0][0], &g->dstate->maxbits[0][0], 2 * kMaxT * 16, ncclUint64, ncclMax,
                      g->comm, g->stream));
-  finalize_kernel<<<1, 32, 0, g->stream>>>(ctl);
+  IterCtl c = ctl;
+  c.join = g->djoin;
+  c.join_mode = join_mode_of(g);
+  finalize_kernel<<<1, 32, 0, g->stream>>>(c);
   CU(cudaGetLastError());
   g->st.kernel_launches += 1;
+  if (c.join_mode == 2) {  // lockstep: everyone published before anyone combines
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));
+    c.join_mode = 3;
+    finalize_kernel<<<1, 32, 0, g->stream>>>(c);
+    CU(cudaGetLastError());
+    g->st.kernel_launches += 1;
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));  // the published slots are read before the next pass can overwrite them
+  }
   return SOR_OK;
 }
 
-bool single_part(const sor_grid* g) { return g->slabs.size() == 1 && g->nranks == 1; }
+// Device-initiated halo exchange: the link of slab s for a pass src -> dst.
+HaloLink make_link(sor_grid* g, const Slab& s, int src, int dst) {
+  HaloLink L{};
+  if (!g->push) return L;
+  L.on = 1;
+  L.H = g->H;
+  L.seq = g->seq;
+  const PlaneInfo& pi = g->pinfo[src];
+  L.need = pi.wseq;
+  L.pg = pi.pg;
+  L.pw = pi.pw;
+  L.pgh = pi.pgh;
+  L.pn = pi.pn;
+  auto off = [&](const Neighbour& nb) -> long long {
+    return (long long)(((intptr_t)nb.plane[dst] - (intptr_t)s.plane[dst]) / (intptr_t)g->esz) +
+           (long long)(s.g0 - nb.g0) * g->pitch;
+  };
+  if (s.up.ok) {
+    L.up_off = off(s.up);
+    L.rel_up = s.up.fbot;
+    L.acq_top = s.ftop;
+  }
+  if (s.dn.ok) {
+    L.dn_off = off(s.dn);
+    L.rel_dn = s.dn.ftop;
+    L.acq_bot = s.fbot;
+  }
+  return L;
+}
+
+int strips_of(const sor_grid* g, int s0, int wc, int ghost) {
+  const int64_t wout = wc - 2 * ghost;
+  return (int)((g->cols + 1 - (s0 + ghost) + wout - 1) / wout);
+}
+
+void record_layout(sor_grid* g, int dst, int s0, int wc, int ghost, int nstrips) {
+  PlaneInfo& pi = g->pinfo[dst];
+  pi.pg = s0 + ghost;
+  pi.pw = wc - 2 * ghost;
+  pi.pgh = ghost;
+  pi.pn = nstrips;
+}
 
 // ------------------------------------------------------------------ K1
 template <typename R>
@@ -538,8 +923,6 @@ int k1_iteration(sor_grid* g, R w, IterCtl ctl) {
 }
 
 // ------------------------------------------------------------------ K3/K4
-template <typename R>
-constexpr int wave_nst() { return 14; }
 
 // ------------------------------------------------------------------ tiles
 // One warp (pair) per tile = (strip, band of owned rows).  A tile runs whole
@@ -663,6 +1046,27 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int w
     }
     for (int w = 0; w < nstrips; ++w) split_strip(w, cost, &tl);
   }
+  if (g->push) {
+    // one pushing tile per strip and side (HaloLink): the first band of each
+    // strip holds the slab's first H rows, the last band its last H rows
+    const int64_t need = std::min<int64_t>(g->H, s.g_hi - s.g_lo);
+    std::map<int, std::vector<int4>> by;
+    for (const int4& x : tl) by[x.x].push_back(x);
+    tl.clear();
+    for (auto& kv : by) {
+      auto& v = kv.second;
+      std::sort(v.begin(), v.end(), [](const int4& x, const int4& y) { return x.y < y.y; });
+      while (v.size() > 1 && v.front().z - v.front().y < need) {
+        v[1].y = v[0].y;
+        v.erase(v.begin());
+      }
+      while (v.size() > 1 && v.back().z - v.back().y < need) {
+        v[v.size() - 2].z = v.back().z;
+        v.pop_back();
+      }
+      for (auto& x : v) tl.push_back(x);
+    }
+  }
   // row-major order: warps running together stream neighbouring strips of the
   // same rows (shared ghost columns hit in L2, DRAM pages stay open)
   std::stable_sort(tl.begin(), tl.end(),
@@ -679,85 +1083,15 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int w
   return SOR_OK;
 }
 
-// Programmatic dependent launch between consecutive wave kernels (one slab:
-// no NCCL or copy between them); SOR_NO_PDL=1 disables it.
-bool wave_pdl(const sor_grid* g) {
+// Programmatic dependent launch between consecutive wave kernels (one slab,
+// or slabs that push their halos: no NCCL or copy between two launches), for
+// one-wave launches only (in a multi-wave launch the next grid's early CTAs
+// would hold slots its own tail needs: measured C5 -0.5%, C3 +2%).
+// SOR_NO_PDL=1 disables it.
+bool wave_pdl(const sor_grid* g, unsigned blocks, int occ) {
   static int off = -1;
   if (off < 0) off = getenv("SOR_NO_PDL") ? 1 : 0;
-  return !off && g->slabs.size() == 1 && g->nranks == 1;
-}
-
-// Split mode (a warp pair per tile, stages divided between the two warps) for
-// T >= 2 unless SOR_WAVE_SPLIT=0 (with -DSOR_WAVE_NOSPLIT_VARIANTS).
-[[maybe_unused]] bool wave_split(int T) {
-  static int sp = -1;
-  if (sp < 0) {
-    const char* e = getenv("SOR_WAVE_SPLIT");
-    sp = e ? atoi(e) : 1;
-  }
-  return sp != 0 && T >= 2;
-}
-
-template <typename R, int T, int CK, bool SPLIT, int NC>
-int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
-  constexpr int NST = wave_nst<R>();
-  constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
-  constexpr int per_cta = wave_tiles_per_cta(SPLIT);
-  static int occ = 0;  // resident CTAs/SM for this instance
-  if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT, NC>, kWaveWarps * 32, smem);
-    if (occ <= 0) occ = 1;
-  }
-  WaveArgs<R> a;
-  a.src = col0<R>(s.plane[g->cur]);
-  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
-  a.pitch = g->pitch;
-  a.g0 = s.g0;
-  a.rows = g->rows;
-  a.cols = g->cols;
-  a.r_lo = s.g_lo;
-  a.r_hi = s.g_hi;
-  a.w = w;
-  a.s0 = -4 * ((2 * T + 3) / 4);
-  const int slab_idx = (int)(&s - &g->slabs[0]);
-  std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
-  a.tiles = tt.first;
-  a.ntiles = tt.second;
-  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta) + (ctl.defer ? 1 : 0);
-  IterCtl c = ctl;
-  c.finalize = fused_fin ? 1 : 0;
-  c.nparts = blocks;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kWaveWarps * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = g->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  // PDL only for one-wave launches: in a multi-wave launch the next grid's
-  // early CTAs would hold slots its own tail needs (measured: C5 -0.5%, C3 +2%)
-  cfg.numAttrs = (wave_pdl(g) && blocks <= (unsigned)(occ * g->nsm)) ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC>, a, c, s.tmap[g->cur]));
-  g->st.kernel_launches += 1;
-  return SOR_OK;
-}
-
-template <typename R, int T, int CK>
-int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
-  // 4 columns per lane: wider lanes (NC = 6, 8; bitwise equal) measured
-  // slower on B200 at every T (fewer resident warps outweigh the extra ILP)
-  // T >= 2: warp pairs (split); the single-warp variant is built only with
-  // -DSOR_WAVE_NOSPLIT_VARIANTS (SOR_WAVE_SPLIT=0 then selects it)
-#ifdef SOR_WAVE_NOSPLIT_VARIANTS
-  if (T >= 2 && wave_split(T)) return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
-  return launch_wave_TS<R, T, CK, false, kWaveNC>(g, s, w, ctl, fused_fin);
-#else
-  return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
-#endif
+  return !off && (single_part(g) || g->push) && !g->lockstep && blocks <= (unsigned)(occ * g->nsm);
 }
 
 template <typename R, int CK>
@@ -770,53 +1104,6 @@ int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool
     case 4: return launch_wave_T<R, 4, CK>(g, s, w, ctl, fused_fin);
   }
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
-}
-
-// Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
-template <typename R, int T, int CK>
-int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {
-  constexpr int NST = wave_nst<R>();
-  constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST, kWaveNC>();
-  constexpr int G = jacobi_ghost(T);
-  static int occ = 0;
-  if (occ == 0) {
-    CU(cudaFuncSetAttribute(jacobi_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
-    if (occ <= 0) occ = 1;
-  }
-  WaveArgs<R> a;
-  a.src = col0<R>(s.plane[g->cur]);
-  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
-  a.pitch = g->pitch;
-  a.g0 = s.g0;
-  a.rows = g->rows;
-  a.cols = g->cols;
-  a.r_lo = s.g_lo;
-  a.r_hi = s.g_hi;
-  a.w = R(1);
-  a.s0 = -4 * ((G + 3) / 4);
-  const int slab_idx = (int)(&s - &g->slabs[0]);
-  std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, G, T, wave_cols<kWaveNC>(), occ * kWaveWarps, false, a.s0, &tt));
-  a.tiles = tt.first;
-  a.ntiles = tt.second;
-  const unsigned blocks = (unsigned)((a.ntiles + kWaveWarps - 1) / kWaveWarps) + (ctl.defer ? 1 : 0);
-  IterCtl c = ctl;
-  c.finalize = fused_fin ? 1 : 0;
-  c.nparts = blocks;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kWaveWarps * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = g->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = (wave_pdl(g) && blocks <= (unsigned)(occ * g->nsm)) ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK>, a, c, s.tmap[g->cur]));
-  g->st.kernel_launches += 1;
-  return SOR_OK;
 }
 
 template <typename R, int CK>
@@ -834,37 +1121,60 @@ int launch_jacobi(sor_grid* g, const Slab& s, int T, const IterCtl& ctl, bool fu
 template <typename R>
 int wave_pass(sor_grid* g, R w, IterCtl ctl) {
   const int T = ctl.T;
+  const int need_rows = g->method == 1 ? T : 2 * T;  // halo rows the pass reads
   const bool fused_fin = single_part(g) && ctl.ck != 0 && !ctl.defer;
-  if (!single_part(g) && g->halo_valid < 2 * T) TRY(exchange(g, g->cur, 2 * T));
-  for (auto& s : g->slabs) {
+  if (!single_part(g) && g->halo_valid < need_rows) TRY(exchange(g, g->cur, 2 * T));
+  g->seq += 1;
+  ctl.seq = g->seq;
+  ctl.join = g->djoin;
+  ctl.join_mode = join_mode_of(g);
+  for (size_t k = 0; k < g->slabs.size(); ++k) {
+    const Slab& s = g->slabs[k];
+    IterCtl c = ctl;
+    if (k > 0) {  // the deferred decision runs in the first slab's launch only
+      c.defer = 0;
+      c.prev_valid = 0;
+    }
     if (g->method == 1) {  // Jacobi: exact maxima only (ck 1 or 2)
-      if (ctl.ck >= 2)
-        TRY((launch_jacobi<R, 2>(g, s, T, ctl, fused_fin)));
-      else if (ctl.ck == 1)
-        TRY((launch_jacobi<R, 1>(g, s, T, ctl, fused_fin)));
+      if (c.ck >= 2)
+        TRY((launch_jacobi<R, 2>(g, s, T, c, fused_fin)));
+      else if (c.ck == 1)
+        TRY((launch_jacobi<R, 1>(g, s, T, c, fused_fin)));
       else
-        TRY((launch_jacobi<R, 0>(g, s, T, ctl, fused_fin)));
+        TRY((launch_jacobi<R, 0>(g, s, T, c, fused_fin)));
       continue;
     }
-    if (ctl.ck == 4)
-      TRY((launch_wave<R, 4>(g, s, T, w, ctl, fused_fin)));
-    else if (ctl.ck == 3)
-      TRY((launch_wave<R, 3>(g, s, T, w, ctl, fused_fin)));
-    else if (ctl.ck == 2)
-      TRY((launch_wave<R, 2>(g, s, T, w, ctl, fused_fin)));
-    else if (ctl.ck == 1)
-      TRY((launch_wave<R, 1>(g, s, T, w, ctl, fused_fin)));
+    if (c.ck == 4)
+      TRY((launch_wave<R, 4>(g, s, T, w, c, fused_fin)));
+    else if (c.ck == 3)
+      TRY((launch_wave<R, 3>(g, s, T, w, c, fused_fin)));
+    else if (c.ck == 2)
+      TRY((launch_wave<R, 2>(g, s, T, w, c, fused_fin)));
+    else if (c.ck == 1)
+      TRY((launch_wave<R, 1>(g, s, T, w, c, fused_fin)));
     else
-      TRY((launch_wave<R, 0>(g, s, T, w, ctl, fused_fin)));
+      TRY((launch_wave<R, 0>(g, s, T, w, c, fused_fin)));
   }
   const int src = g->cur;
+  const PlaneInfo spi = g->pinfo[src];
   g->cur = g->nxt(src);
   g->st.half_sweeps += g->method == 1 ? T : 2 * T;  // Jacobi: one sweep per iteration
   g->st.hbm_passes += 1;
-  TRY(exchange(g, g->cur, 2 * T));
-  g->halo_valid = 2 * T;
+  if (g->push) {
+    // the pass pushed its first/last H rows into the neighbours' halos
+    g->pinfo[g->cur].wseq = g->seq;
+    g->halo_valid = g->H;
+    g->st.halo_exchanges += single_part(g) ? 0 : 1;
+  } else {
+    TRY(exchange(g, g->cur, 2 * T));
+    g->halo_valid = 2 * T;
+  }
+  if (g->lockstep) {  // ranks sharing a GPU: the pass is complete everywhere before the next one
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));
+  }
   if (ctl.ck && !fused_fin && !ctl.defer) TRY(join_and_finalize(g, ctl));
-  g->pass_ends.push_back({ctl.k_last, src, g->cur, T});
+  g->pass_ends.push_back({ctl.k_last, src, g->cur, T, spi, g->pinfo[g->cur]});
   return SOR_OK;
 }
 
@@ -886,6 +1196,9 @@ size_t k5_limit_bytes() { return 200 * 1024; }
 
 // ------------------------------------------------------------------ drivers
 int begin_call(sor_grid* g) {
+  // dist-IPC: every rank finished its previous call before anyone pushes
+  // into a neighbour's planes again
+  TRY(dist_barrier(g));
   g->st.kernel_launches = 0;
   g->st.half_sweeps = 0;
   g->st.halo_exchanges = 0;
@@ -908,6 +1221,8 @@ int end_call(sor_grid* g, DevState* out) {
   CU(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
   g->elapsed_ms = ms;
   g->have_elapsed = true;
+  if (g->hstate[0].halo_timeout)
+    return set_error(g, SOR_E_CUDA, "halo/join wait timed out (a peer rank never released its rows)");
   if (out) *out = g->hstate[0];
   return SOR_OK;
 }
@@ -972,6 +1287,7 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
         c.prev_T = g->prev_T;
         c.prev_ck = g->prev_ck;
         c.prev_set = g->prev_set;
+        c.prev_seq = g->prev_seq;
         g->prev_valid = false;
         c.set = g->next_set;
         if (c.ck) {
@@ -980,6 +1296,7 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
           g->prev_T = c.T;
           g->prev_ck = c.ck;
           g->prev_set = c.set;
+          g->prev_seq = g->seq + 1;  // the sequence number wave_pass gives this pass
           g->next_set ^= 1;
         }
       }
@@ -1018,6 +1335,8 @@ int iterate_impl(sor_grid* g, double omega, int64_t iters, double* last) {
 int read_state(sor_grid* g, DevState* out) {
   CU(cudaMemcpyAsync(&g->hstate[0], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
   CU(cudaStreamSynchronize(g->stream));
+  if (g->hstate[0].halo_timeout)
+    return set_error(g, SOR_E_CUDA, "halo/join wait timed out (a peer rank never released its rows)");
   *out = g->hstate[0];
   return SOR_OK;
 }
@@ -1039,8 +1358,12 @@ bool find_pass(const sor_grid* g, int64_t k, sor_grid::PassRec* out) {
 // (ck=2, solve semantics).  Leaves g->cur on the plane holding the result.
 template <typename R>
 int rerun_pass(sor_grid* g, R w, const IterCtl& base, const sor_grid::PassRec& pr, int depth, int ck, DevState* out) {
+  // dist-IPC: the neighbours' speculative passes that read the planes this
+  // re-run pushes into are complete (their streams drained, barrier)
+  TRY(dist_barrier(g));
   CU(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
   g->cur = pr.src;  // writes the pass's own destination plane again
+  g->pinfo[pr.src] = pr.spi;  // passes after it exited early but were booked
   IterCtl c = base;
   c.k_last = pr.k_last - pr.T + depth;
   c.T = depth;
@@ -1052,27 +1375,47 @@ int rerun_pass(sor_grid* g, R w, const IterCtl& base, const sor_grid::PassRec& p
   return read_state(g, out);
 }
 
-// Third plane for the deferred stop test (single slab): allocated once, a copy
-// of the current plane (ring, padding); false if memory is short.
+// Third plane for the deferred stop test: allocated once, a copy of the
+// current plane (ring, padding); false if memory is short or the handle's
+// ranks cannot defer (NCCL transport: host-side exchanges between passes;
+// lockstep IPC ranks: the decision needs a host barrier).  Dist-IPC handles
+// allocate it at creation (the neighbours map it).
 bool ensure_third_plane(sor_grid* g) {
-  if (g->nplanes == 3) return true;
-  if (!single_part(g)) return false;
   static int off = -1;
   if (off < 0) off = getenv("SOR_NO_DEFER") ? 1 : 0;
-  if (off) return false;
-  Slab& s = g->slabs[0];
-  const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
-  if (cudaMalloc(&s.plane[2], bytes) != cudaSuccess) {
-    cudaGetLastError();
-    s.plane[2] = nullptr;
+  if (off || g->lockstep || g->transport == Transport::Nccl) return false;
+  if (g->nplanes == 3) return true;
+  if (!single_part(g) && !g->push) return false;
+  bool ok = true;
+  for (auto& s : g->slabs) {
+    const size_t bytes = (size_t)s.nstore * g->pitch * g->esz;
+    if (cudaMalloc(&s.plane[2], bytes) != cudaSuccess) {
+      cudaGetLastError();
+      s.plane[2] = nullptr;
+      ok = false;
+      break;
+    }
+    if (cudaMemcpyAsync(s.plane[2], s.plane[g->cur], bytes, cudaMemcpyDeviceToDevice, g->stream) != cudaSuccess ||
+        make_tmaps(g, s, 2) != SOR_OK) {
+      ok = false;
+      break;
+    }
+  }
+  if (!ok) {
+    cudaStreamSynchronize(g->stream);
+    for (auto& s : g->slabs)
+      if (s.plane[2]) {
+        cudaFree(s.plane[2]);
+        s.plane[2] = nullptr;
+      }
     return false;
   }
-  if (cudaMemcpyAsync(s.plane[2], s.plane[g->cur], bytes, cudaMemcpyDeviceToDevice, g->stream) != cudaSuccess ||
-      make_tmaps(g, s, 2) != SOR_OK) {
-    cudaFree(s.plane[2]);
-    s.plane[2] = nullptr;
-    return false;
+  const int n = (int)g->slabs.size();
+  for (int k = 0; k < n; ++k) {
+    if (k > 0) g->slabs[k].up.plane[2] = g->slabs[k - 1].plane[2];
+    if (k + 1 < n) g->slabs[k].dn.plane[2] = g->slabs[k + 1].plane[2];
   }
+  g->pinfo[2] = g->pinfo[g->cur];
   g->nplanes = 3;
   return true;
 }
@@ -1141,7 +1484,12 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
                            g->stream));
         CU(cudaEventRecord(g->poll_ev[b & 1], g->stream));
         kk = k_to + 1;
-        if (b >= 1) {
+        if (g->transport == Transport::Nccl) {
+          // NCCL ranks must enqueue the same collectives: decide on this
+          // batch's state (identical on every rank after the allreduce)
+          CU(cudaEventSynchronize(g->poll_ev[b & 1]));
+          if (g->hstate[b & 1].stop) break;
+        } else if (b >= 1) {
           CU(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
           if (g->hstate[(b - 1) & 1].stop) break;
         }
@@ -1154,6 +1502,9 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         c.T = g->prev_T;
         c.ck = g->prev_ck;
         c.set = g->prev_set;
+        c.seq = g->prev_seq;
+        c.join = g->djoin;
+        c.join_mode = join_mode_of(g);
         c.defer = 0;
         finalize_kernel<<<1, 32, 0, g->stream>>>(c);
         CU(cudaGetLastError());
@@ -1161,6 +1512,9 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         g->prev_valid = false;
       }
       TRY(read_state(g, &hs));
+      // dist-IPC: ranks may have enqueued different numbers of (early-exit)
+      // passes after the stop; agree on the sequence counter again
+      TRY(sync_seq(g));
       checks += hs.checks;
       if (g->kernel == SOR_KERNEL_NATURAL) {  // in place, exact checks: nothing to redo
         converged = hs.converged != 0;
@@ -1230,6 +1584,7 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
         maxc = fin.max_change;
       } else {
         g->cur = pr.dst;  // passes end on checked iterations
+        g->pinfo[pr.dst] = pr.dpi;
         maxc = hs.max_change;
       }
       break;
@@ -1250,6 +1605,106 @@ int validate_omega(double omega) {
   return SOR_OK;
 }
 
+// ---- gather (download) of global rows [ra, rb) into out (row ra at out)
+int gather_rows(sor_grid* g, int64_t ra, int64_t rb, double* out) {
+  const int64_t w = g->cols + 2;
+  double* base = out ? out - ra * w : nullptr;  // store_rows indexes by global row
+  auto span_of = [&](int q, int nq, int64_t lo, int64_t hi, int64_t* a, int64_t* b) {
+    *a = std::max(ra, q == 0 ? (int64_t)0 : lo);
+    *b = std::min(rb, q == nq - 1 ? g->rows + 2 : hi);
+  };
+  if (g->mode != Mode::Dist) {
+    CU(cudaStreamSynchronize(g->stream));
+    const int n = (int)g->slabs.size();
+    for (int k = 0; k < n; ++k) {
+      const Slab& s = g->slabs[k];
+      int64_t sa, sb;
+      span_of(k, n, s.g_lo, s.g_hi, &sa, &sb);
+      if (sa < sb) TRY(store_rows(g, s, g->cur, base, sa, sb));
+    }
+    CU(cudaStreamSynchronize(g->stream));
+    return SOR_OK;
+  }
+  if (g->transport == Transport::Ipc) {  // rank 0 reads every rank's plane
+    CU(cudaStreamSynchronize(g->stream));
+    TRY(shm_barrier(g));
+    int rc = SOR_OK;
+    if (g->rank == 0) {
+      for (int q = 0; q < g->nranks && rc == SOR_OK; ++q) {
+        const Slab& s = g->rslabs[q];
+        int64_t sa, sb;
+        span_of(q, g->nranks, s.g_lo, s.g_hi, &sa, &sb);
+        if (sa < sb) rc = store_rows(g, s, g->cur, base, sa, sb);
+      }
+      if (rc == SOR_OK && cudaStreamSynchronize(g->stream) != cudaSuccess)
+        rc = set_error(g, SOR_E_CUDA, "gather: sync failed");
+    }
+    TRY(shm_barrier(g));  // nobody changes its planes before rank 0 has read them
+    return rc;
+  }
+  // NCCL: every rank sends its part to rank 0 (whole storage rows)
+  const size_t row_bytes = (size_t)g->pitch * g->esz;
+  const Slab& me = g->slabs[0];
+  CU(cudaStreamSynchronize(g->stream));
+  if (g->rank != 0) {
+    int64_t sa, sb;
+    span_of(g->rank, g->nranks, me.g_lo, me.g_hi, &sa, &sb);
+    if (sa < sb)
+      NC(ncclSend((char*)me.plane[g->cur] + (sa - me.g0) * row_bytes, (sb - sa) * row_bytes, ncclUint8, 0, g->comm,
+                  g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    return SOR_OK;
+  }
+  int64_t sa, sb;
+  span_of(0, g->nranks, me.g_lo, me.g_hi, &sa, &sb);
+  if (sa < sb) TRY(store_rows(g, me, g->cur, base, sa, sb));
+  int64_t maxr = 0;
+  for (int p = 1; p < g->nranks; ++p) {
+    int64_t lo, hi, a, b;
+    partition(g->rows, g->nranks, p, &lo, &hi);
+    span_of(p, g->nranks, lo, hi, &a, &b);
+    maxr = std::max(maxr, b - a);
+  }
+  void* tmp = nullptr;
+  if (maxr > 0) CU(cudaMalloc(&tmp, (size_t)maxr * row_bytes));
+  int rc = SOR_OK;
+  for (int p = 1; p < g->nranks && rc == SOR_OK; ++p) {
+    int64_t lo, hi, a, b;
+    partition(g->rows, g->nranks, p, &lo, &hi);
+    span_of(p, g->nranks, lo, hi, &a, &b);
+    if (a >= b) continue;
+    const ncclResult_t r = ncclRecv(tmp, (b - a) * row_bytes, ncclUint8, p, g->comm, g->stream);
+    if (r != ncclSuccess) {
+      rc = set_error(g, SOR_E_NCCL, "gather: %s", ncclGetErrorString(r));
+      break;
+    }
+    Slab t;  // the received rows as a slab whose storage row 0 is global row a
+    t.g0 = a;
+    t.nstore = b - a;
+    t.plane[0] = tmp;
+    rc = store_rows(g, t, 0, base, a, b);
+    if (rc == SOR_OK && cudaStreamSynchronize(g->stream) != cudaSuccess)
+      rc = set_error(g, SOR_E_CUDA, "gather: sync failed");
+  }
+  cudaStreamSynchronize(g->stream);
+  if (tmp) cudaFree(tmp);
+  return rc;
+}
+
+// Every ABI call on a handle runs on the handle's device and restores the
+// caller's current device afterwards.
+struct DevGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DevGuard(const sor_grid* g) {
+    if (g && cudaGetDevice(&prev) == cudaSuccess && prev != g->device)
+      changed = cudaSetDevice(g->device) == cudaSuccess;
+  }
+  ~DevGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -1265,21 +1720,26 @@ int sor_partition_rows(int64_t rows, int P, int p, int64_t* lo, int64_t* hi) {
 }
 
 int sor_create(sor_grid** out, int64_t N, const double* init, sor_dtype dt) {
-  return create_common(out, N, N, init, dt, Mode::Single, 1, 0, 1, 0, nullptr);
+  return create_common(out, N, N, init, dt, Mode::Single, 1, 0, 1, 0, nullptr, Transport::None);
 }
 
 int sor_create_rect(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt) {
-  return create_common(out, rows, cols, init, dt, Mode::Single, 1, 0, 1, 0, nullptr);
+  return create_common(out, rows, cols, init, dt, Mode::Single, 1, 0, 1, 0, nullptr, Transport::None);
 }
 
 int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
                        int nslabs) {
-  return create_common(out, rows, cols, init, dt, Mode::Virtual, nslabs, 0, 1, 0, nullptr);
+  return create_common(out, rows, cols, init, dt, Mode::Virtual, nslabs, 0, 1, 0, nullptr, Transport::None);
 }
 
 int sor_create_dist(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
                     int rank, int nranks, int device, const void* nccl_id) {
-  return create_common(out, rows, cols, init, dt, Mode::Dist, 1, rank, nranks, device, nccl_id);
+  return create_common(out, rows, cols, init, dt, Mode::Dist, 1, rank, nranks, device, nccl_id, Transport::Nccl);
+}
+
+int sor_create_dist_ipc(sor_grid** out, int64_t rows, int64_t cols, const double* init, sor_dtype dt,
+                        int rank, int nranks, int device, const void* ipc_id) {
+  return create_common(out, rows, cols, init, dt, Mode::Dist, 1, rank, nranks, device, ipc_id, Transport::Ipc);
 }
 
 int sor_nccl_unique_id(void* out128) {
@@ -1291,26 +1751,45 @@ int sor_nccl_unique_id(void* out128) {
   return SOR_OK;
 }
 
+int sor_ipc_unique_id(void* out128) {
+  if (!out128) return set_error(nullptr, SOR_E_INVAL, "NULL output");
+  std::random_device rd;
+  const unsigned long long r = ((unsigned long long)rd() << 32) ^ rd() ^
+                               (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count();
+  char buf[128];
+  memset(buf, 0, sizeof buf);
+  snprintf(buf, sizeof buf, "/sorb-%d-%016llx", (int)getpid(), r);
+  memcpy(out128, buf, sizeof buf);
+  return SOR_OK;
+}
+
 int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
   TRY(usable(g));
   switch (kernel) {
     case SOR_KERNEL_NATURAL:
+      if (g->transport == Transport::Ipc)
+        return set_error(nullptr, SOR_E_UNSUPPORTED, "SOR_KERNEL_NATURAL is not available on dist-IPC handles");
+      g->kernel = kernel;
+      g->tdepth = 1;
+      break;
     case SOR_KERNEL_FUSED:
       g->kernel = kernel;
       g->tdepth = 1;
       break;
-    case SOR_KERNEL_TEMPORAL:
-      if (temporal_depth < 1 || temporal_depth > 4)
-        return set_error(nullptr, SOR_E_INVAL, "temporal_depth must be in [1,4], got %d", temporal_depth);
-      if (g->slabs.size() > 1 || g->nranks > 1) {
-        for (auto& s : g->slabs)
-          if (s.g_hi - s.g_lo < 2 * temporal_depth)
-            return set_error(nullptr, SOR_E_INVAL, "slab of %lld rows too thin for T=%d",
-                             (long long)(s.g_hi - s.g_lo), temporal_depth);
-      }
+    case SOR_KERNEL_TEMPORAL: {
+      if (temporal_depth < 1 || temporal_depth > kMaxT)
+        return set_error(nullptr, SOR_E_INVAL, "temporal_depth must be in [1,%d], got %d", kMaxT, temporal_depth);
+      // the thinnest slab of any rank (sizes differ by at most one row)
+      int64_t thin = g->rows;
+      for (auto& s : g->slabs) thin = std::min(thin, s.g_hi - s.g_lo);
+      if (g->nranks > 1) thin = g->rows / g->nranks;
+      if ((g->slabs.size() > 1 || g->nranks > 1) && thin < 2 * temporal_depth)
+        return set_error(nullptr, SOR_E_INVAL, "slab of %lld rows too thin for T=%d", (long long)thin,
+                         temporal_depth);
       g->kernel = kernel;
       g->tdepth = temporal_depth;
       break;
+    }
     case SOR_KERNEL_SMALL: {
       if (!single_part(g))
         return set_error(nullptr, SOR_E_UNSUPPORTED, "SOR_KERNEL_SMALL needs a single-slab grid");
@@ -1331,6 +1810,7 @@ int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
 
 int sor_set_stream(sor_grid* g, void* cuda_stream) {
   TRY(usable(g));
+  DevGuard dg(g);
   CU(cudaStreamSynchronize(g->stream));
   g->stream = cuda_stream ? (cudaStream_t)cuda_stream : g->own_stream;
   return SOR_OK;
@@ -1340,6 +1820,7 @@ int sor_iterate(sor_grid* g, double omega, int64_t iters, double* last_max_chang
   TRY(usable(g));
   TRY(validate_omega(omega));
   if (iters < 0) return set_error(nullptr, SOR_E_INVAL, "iters must be >= 0");
+  DevGuard dg(g);
   if (g->dt == SOR_F64) return iterate_impl<double>(g, omega, iters, last_max_change);
   return iterate_impl<float>(g, omega, iters, last_max_change);
 }
@@ -1352,6 +1833,7 @@ int sor_solve(sor_grid* g, double omega, double tol, int64_t maxit, int64_t chec
   if (maxit < 1) return set_error(nullptr, SOR_E_INVAL, "maxit must be >= 1");
   if (check_every < 1 || check_every > maxit)
     return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
+  DevGuard dg(g);
   if (g->dt == SOR_F64) return solve_impl<double>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
   return solve_impl<float>(g, omega, tol, maxit, check_every, iters_out, max_change_out);
 }
@@ -1373,6 +1855,7 @@ int sor_jacobi_iterate(sor_grid* g, int64_t iters, double* last_max_change) {
   TRY(usable(g));
   TRY(jacobi_usable(g));
   if (iters < 0) return set_error(nullptr, SOR_E_INVAL, "iters must be >= 0");
+  DevGuard dg(g);
   MethodGuard mg(g);
   if (g->dt == SOR_F64) return iterate_impl<double>(g, 1.0, iters, last_max_change);
   return iterate_impl<float>(g, 1.0, iters, last_max_change);
@@ -1386,6 +1869,7 @@ int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every
   if (maxit < 1) return set_error(nullptr, SOR_E_INVAL, "maxit must be >= 1");
   if (check_every < 1 || check_every > maxit)
     return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
+  DevGuard dg(g);
   MethodGuard mg(g);
   if (g->dt == SOR_F64) return solve_impl<double>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
   return solve_impl<float>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
@@ -1393,80 +1877,28 @@ int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every
 
 int sor_download(sor_grid* g, double* out) {
   TRY(usable(g));
-  if (g->mode != Mode::Dist || g->rank == 0) {
-    if (!out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
-  }
-  CU(cudaStreamSynchronize(g->stream));
-  if (g->mode != Mode::Dist) {
-    const int n = (int)g->slabs.size();
-    for (int k = 0; k < n; ++k) {
-      const Slab& s = g->slabs[k];
-      const int64_t ga = k == 0 ? 0 : s.g_lo;
-      const int64_t gb = k == n - 1 ? g->rows + 2 : s.g_hi;
-      TRY(store_rows(g, s, g->cur, out, ga, gb));
-    }
-    CU(cudaStreamSynchronize(g->stream));
-    return SOR_OK;
-  }
-  // dist: rank 0 gathers every slab (owned rows; first/last include the ring)
-  const Slab& s = g->slabs[0];
-  const size_t row_bytes = (size_t)g->pitch * g->esz;
-  const int64_t my_a = g->rank == 0 ? 0 : s.g_lo;
-  const int64_t my_b = g->rank == g->nranks - 1 ? g->rows + 2 : s.g_hi;
-  if (g->rank == 0) {
-    TRY(store_rows(g, s, g->cur, out, my_a, my_b));
-    for (int p = 1; p < g->nranks; ++p) {
-      int64_t lo, hi;
-      partition(g->rows, g->nranks, p, &lo, &hi);
-      const int64_t a = lo, b = p == g->nranks - 1 ? g->rows + 2 : hi;
-      // receive into a temporary slab-shaped buffer, then unpack
-      void* tmp = nullptr;
-      CU(cudaMalloc(&tmp, (size_t)(b - a) * row_bytes));
-      NC(ncclRecv(tmp, (b - a) * row_bytes, ncclUint8, p, g->comm, g->stream));
-      Slab t;
-      t.g0 = a;
-      t.plane[0] = (char*)tmp - 0;  // rows start at global row a
-      t.nstore = b - a;
-      t.plane[1] = t.plane[0];
-      int rc = store_rows(g, t, 0, out, a, b);
-      CU(cudaStreamSynchronize(g->stream));
-      cudaFree(tmp);
-      if (rc < 0) return rc;
-    }
-  } else {
-    NC(ncclSend((char*)s.plane[g->cur] + (my_a - s.g0) * row_bytes, (my_b - my_a) * row_bytes,
-                ncclUint8, 0, g->comm, g->stream));
-  }
-  CU(cudaStreamSynchronize(g->stream));
-  return SOR_OK;
+  if ((g->mode != Mode::Dist || g->rank == 0) && !out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
+  DevGuard dg(g);
+  if (out && is_device_ptr(out)) CU(cudaDeviceSynchronize());  // the caller's pending reads of `out`
+  return gather_rows(g, 0, g->rows + 2, g->mode == Mode::Dist && g->rank != 0 ? nullptr : out);
 }
 
 int sor_download_rows(sor_grid* g, int64_t row_a, int64_t row_b, double* out) {
   TRY(usable(g));
-  if (g->mode == Mode::Dist) return set_error(nullptr, SOR_E_UNSUPPORTED, "download_rows: not on dist handles");
-  if (!out || row_a < 0 || row_b > g->rows + 2 || row_a >= row_b)
-    return set_error(nullptr, SOR_E_INVAL, "download_rows: need 0 <= row_a < row_b <= rows+2 and out");
-  CU(cudaStreamSynchronize(g->stream));
-  const int n = (int)g->slabs.size();
-  const int64_t w = g->cols + 2;
-  for (int k = 0; k < n; ++k) {
-    const Slab& s = g->slabs[k];
-    const int64_t sa = std::max(row_a, k == 0 ? (int64_t)0 : s.g_lo);
-    const int64_t sb = std::min(row_b, k == n - 1 ? g->rows + 2 : s.g_hi);
-    if (sa >= sb) continue;
-    // store_rows indexes `out` by global row; shift the base accordingly
-    TRY(store_rows(g, s, g->cur, out - row_a * w, sa, sb));
-  }
-  CU(cudaStreamSynchronize(g->stream));
-  return SOR_OK;
+  if (row_a < 0 || row_b > g->rows + 2 || row_a >= row_b)
+    return set_error(nullptr, SOR_E_INVAL, "download_rows: need 0 <= row_a < row_b <= rows+2");
+  if ((g->mode != Mode::Dist || g->rank == 0) && !out) return set_error(nullptr, SOR_E_INVAL, "out is NULL");
+  DevGuard dg(g);
+  if (out && is_device_ptr(out)) CU(cudaDeviceSynchronize());
+  return gather_rows(g, row_a, row_b, g->mode == Mode::Dist && g->rank != 0 ? nullptr : out);
 }
 
 int sor_reset(sor_grid* g, const double* init) {
   TRY(usable(g));
-  if (!init) return set_error(nullptr, SOR_E_INVAL, "init is NULL");
-  const bool on_dev = is_device_ptr(init);
-  TRY(check_finite(g, init, (g->rows + 2) * (g->cols + 2), on_dev));
-  return load_all(g, init);
+  DevGuard dg(g);
+  CU(cudaStreamSynchronize(g->stream));
+  TRY(dist_barrier(g));  // no rank is still running on the planes being reloaded
+  return load_grid(g, init);
 }
 
 int sor_last_elapsed_ms(const sor_grid* g, double* ms) {
@@ -1484,327 +1916,17 @@ int sor_get_stats(const sor_grid* g, sor_stats* out) {
 
 void sor_destroy(sor_grid* g) {
   if (!g) return;
+  DevGuard dg(g);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->transport == Transport::Ipc && g->shm && !g->failed) {
+    // no rank frees memory another rank still pushes into or has mapped
+    if (shm_barrier(g, 60.0) == SOR_OK) {
+      for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
+      g->ipc_opened.clear();
+      shm_barrier(g, 60.0);
+    }
+  }
   free_grid(g);
-}
-
-}  // extern "C"
-
-// ====================================================================== 3-D
-// NEXT-3: 3-D red-black SOR handle (single GPU, K1-form kernels; see
-// k3d_half_sweep).  Loop control as the 2-D natural path: the stop test runs
-// in the last CTA of the checking iteration's black launch, later launches
-// exit early, the host polls one batch behind.
-struct sor3d_grid {
-  int64_t nz = 0, ny = 0, nx = 0;
-  sor_dtype dt = SOR_F64;
-  size_t esz = 8;
-  int64_t pitch = 0;
-  void* plane = nullptr;        // the current iterate
-  void* plane2 = nullptr;       // FUSED kernel: the other plane of the ping-pong
-  // default NATURAL: the fused z-wavefront is bitwise equal but slower on
-  // B200 (f64 57 vs 158 GLUP/s at 512^3: the correctly rounded division on its
-  // per-plane critical path, one CTA barrier per plane)
-  int kernel = SOR_KERNEL_NATURAL;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, poll_ev[2] = {nullptr, nullptr};
-  DevState* dstate = nullptr;
-  DevState* hstate = nullptr;
-  double* scratch = nullptr;
-  bool failed = false, have_elapsed = false;
-  double elapsed_ms = 0.0;
-};
-
-namespace {
-
-int set_error3(sor3d_grid* g, int code, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  g_last_error = buf;
-  if (g && (code == SOR_E_CUDA)) g->failed = true;
-  return code;
-}
-
-#define CU3(call)                                                                      \
-  do {                                                                                 \
-    cudaError_t e_ = (call);                                                           \
-    if (e_ != cudaSuccess)                                                             \
-      return set_error3(g, SOR_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
-  } while (0)
-
-void free3d(sor3d_grid* g) {
-  if (!g) return;
-  if (g->plane) cudaFree(g->plane);
-  if (g->plane2) cudaFree(g->plane2);
-  if (g->dstate) cudaFree(g->dstate);
-  if (g->hstate) cudaFreeHost(g->hstate);
-  if (g->scratch) cudaFree(g->scratch);
-  if (g->ev0) cudaEventDestroy(g->ev0);
-  if (g->ev1) cudaEventDestroy(g->ev1);
-  for (int k = 0; k < 2; ++k)
-    if (g->poll_ev[k]) cudaEventDestroy(g->poll_ev[k]);
-  if (g->stream) cudaStreamDestroy(g->stream);
-  delete g;
-}
-
-// (z, y) rows of the full fp64 array <-> the padded device plane
-int load3d(sor3d_grid* g, const double* init) {
-  const int64_t w = g->nx + 2, nrow = (g->nz + 2) * (g->ny + 2);
-  const size_t bytes = (size_t)nrow * g->pitch * g->esz;
-  CU3(cudaMemsetAsync(g->plane, 0, bytes, g->stream));
-  if (g->dt == SOR_F64) {
-    CU3(cudaMemcpy2DAsync(g->plane, g->pitch * 8, init, w * 8, w * 8, nrow, cudaMemcpyDefault, g->stream));
-  } else {
-    CU3(cudaMemcpyAsync(g->scratch, init, (size_t)nrow * w * 8, cudaMemcpyDefault, g->stream));
-    dim3 grid((unsigned)std::min<int64_t>((w + 255) / 256, 1024), (unsigned)std::min<int64_t>(nrow, 65535));
-    narrow_rows<<<grid, 256, 0, g->stream>>>(g->scratch, w, (float*)g->plane, g->pitch, nrow, w);
-    CU3(cudaGetLastError());
-  }
-  // both planes carry the shell (the fused kernel never writes planes 0, nz+1)
-  CU3(cudaMemcpyAsync(g->plane2, g->plane, bytes, cudaMemcpyDeviceToDevice, g->stream));
-  CU3(cudaStreamSynchronize(g->stream));
-  return SOR_OK;
-}
-
-template <typename R>
-int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
-  if (g->kernel == SOR_KERNEL_FUSED) {
-    dim3 grid((unsigned)((g->nx + 2 + kX3 - 1) / kX3), (unsigned)((g->ny + 2 + kY3 - 1) / kY3));
-    IterCtl c = ctl;
-    c.finalize = ctl.ck ? 1 : 0;
-    c.nparts = grid.x * grid.y;
-    if (ctl.ck)
-      k3d_fused<R, true><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
-                                                             (int)g->nz, (int)g->ny, (int)g->nx, w, c);
-    else
-      k3d_fused<R, false><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
-                                                              (int)g->nz, (int)g->ny, (int)g->nx, w, c);
-    CU3(cudaGetLastError());
-    std::swap(g->plane, g->plane2);
-    return SOR_OK;
-  }
-  const int64_t half = (g->nx + 1) / 2;
-  dim3 grid((unsigned)((half + 255) / 256), (unsigned)g->ny, (unsigned)g->nz);
-  for (int color = 0; color < 2; ++color) {
-    IterCtl c = ctl;
-    c.finalize = (color == 1 && ctl.ck) ? 1 : 0;
-    c.nparts = grid.x * grid.y * grid.z;
-    if (ctl.ck && color == 1)
-      k3d_half_sweep<R, true><<<grid, 256, 0, g->stream>>>((R*)g->plane, g->pitch, (int)g->nz, (int)g->ny,
-                                                           (int)g->nx, color, w, c);
-    else if (ctl.ck)
-      k3d_half_sweep<R, true><<<grid, 256, 0, g->stream>>>((R*)g->plane, g->pitch, (int)g->nz, (int)g->ny,
-                                                           (int)g->nx, color, w, c);
-    else
-      k3d_half_sweep<R, false><<<grid, 256, 0, g->stream>>>((R*)g->plane, g->pitch, (int)g->nz, (int)g->ny,
-                                                            (int)g->nx, color, w, c);
-    CU3(cudaGetLastError());
-  }
-  return SOR_OK;
-}
-
-template <typename R>
-int run3d(sor3d_grid* g, double omega, int solve, int64_t n, double tol, int64_t K, bool want_last,
-          int64_t* iters_out, double* max_out, bool* converged) {
-  CU3(cudaMemsetAsync(g->dstate, 0, sizeof(DevState), g->stream));
-  CU3(cudaEventRecord(g->ev0, g->stream));
-  IterCtl base{};
-  base.st = g->dstate;
-  base.maxit = n;
-  base.K = solve ? K : 1;
-  base.tol = tol;
-  base.solve = solve;
-  base.T = 1;
-  const R w = (R)omega;
-  const int64_t blk = 64;
-  int b = 0;
-  int64_t enq = 0;  // iterations enqueued (launches after a stop exit early)
-  for (int64_t k0 = 1; k0 <= n; k0 += blk) {
-    const int64_t k1 = std::min(n, k0 + blk - 1);
-    for (int64_t k = k0; k <= k1; ++k) {
-      IterCtl c = base;
-      c.k_last = k;
-      c.ck = solve ? (k % K == 0) : (want_last && k == n);
-      TRY(k3d_iteration<R>(g, w, c));
-      ++enq;
-    }
-    if (solve) {
-      CU3(cudaMemcpyAsync(&g->hstate[b & 1], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
-      CU3(cudaEventRecord(g->poll_ev[b & 1], g->stream));
-      if (b >= 1) {
-        CU3(cudaEventSynchronize(g->poll_ev[(b - 1) & 1]));
-        if (g->hstate[(b - 1) & 1].stop) break;
-      }
-      ++b;
-    }
-  }
-  CU3(cudaEventRecord(g->ev1, g->stream));
-  CU3(cudaMemcpyAsync(&g->hstate[0], g->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, g->stream));
-  CU3(cudaStreamSynchronize(g->stream));
-  float ms = 0.f;
-  CU3(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-  g->elapsed_ms = ms;
-  g->have_elapsed = true;
-  const DevState& hs = g->hstate[0];
-  *converged = hs.converged != 0;
-  // the fused kernel swapped planes once per enqueued iteration, but those
-  // after the converging one exited without writing
-  if (g->kernel == SOR_KERNEL_FUSED && solve && hs.converged && ((enq - hs.conv_iter) & 1))
-    std::swap(g->plane, g->plane2);
-  if (iters_out) *iters_out = solve ? (hs.converged ? hs.conv_iter : n) : n;
-  if (max_out) *max_out = (solve || want_last) && n > 0 ? hs.max_change : 0.0;
-  return SOR_OK;
-}
-
-int usable3(sor3d_grid* g) {
-  if (!g) return set_error3(nullptr, SOR_E_INVAL, "handle is NULL");
-  if (g->failed) return set_error3(nullptr, SOR_E_STATE, "handle failed earlier (CUDA error); destroy it");
-  return SOR_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const double* init, sor_dtype dt) {
-  if (!out) return set_error3(nullptr, SOR_E_INVAL, "out is NULL");
-  *out = nullptr;
-  if (!init) return set_error3(nullptr, SOR_E_INVAL, "init is NULL");
-  if (dt != SOR_F64 && dt != SOR_F32) return set_error3(nullptr, SOR_E_INVAL, "bad dtype %d", (int)dt);
-  if (nz < 1 || ny < 1 || nx < 1 || nz > 65535 || ny > 65535 || nx > (1 << 30))
-    return set_error3(nullptr, SOR_E_INVAL, "need 1 <= nz, ny <= 65535 and 1 <= nx");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
-    cudaGetLastError();
-    return set_error3(nullptr, SOR_E_CUDA, "no CUDA device available; libsor has no CPU fallback");
-  }
-  int dev = 0;
-  cudaDeviceProp prop{};
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10)
-    return set_error3(nullptr, SOR_E_CUDA, "libsor.so is built for sm_100a (B200)");
-  const int64_t n = (nz + 2) * (ny + 2) * (nx + 2);
-  const bool on_dev = is_device_ptr(init);
-  if (!on_dev && !host_all_finite(init, n))
-    return set_error3(nullptr, SOR_E_INVAL, "init contains non-finite values");
-  sor3d_grid* g = new sor3d_grid();
-  g->nz = nz;
-  g->ny = ny;
-  g->nx = nx;
-  g->dt = dt;
-  g->esz = dt == SOR_F64 ? 8 : 4;
-  g->pitch = round_up(nx + 2, 32);
-  int rc = SOR_OK;
-  do {
-    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g->poll_ev[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g->poll_ev[1], cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(&g->dstate, sizeof(DevState)) != cudaSuccess ||
-        cudaMallocHost(&g->hstate, 2 * sizeof(DevState)) != cudaSuccess) {
-      rc = set_error3(nullptr, SOR_E_CUDA, "3-D handle setup failed");
-      break;
-    }
-    if (cudaMalloc(&g->plane, (size_t)(nz + 2) * (ny + 2) * g->pitch * g->esz) != cudaSuccess ||
-        cudaMalloc(&g->plane2, (size_t)(nz + 2) * (ny + 2) * g->pitch * g->esz) != cudaSuccess ||
-        (dt == SOR_F32 && cudaMalloc(&g->scratch, (size_t)n * 8) != cudaSuccess)) {
-      cudaGetLastError();
-      rc = set_error3(nullptr, SOR_E_NOMEM, "3-D grid allocation failed");
-      break;
-    }
-    if (on_dev) {  // device-resident init: the same non-finite check on the GPU
-      unsigned int* flag = nullptr;
-      unsigned int bad = 0;
-      if (cudaMalloc(&flag, sizeof(unsigned int)) != cudaSuccess) {
-        rc = set_error3(nullptr, SOR_E_NOMEM, "flag allocation failed");
-        break;
-      }
-      cudaMemsetAsync(flag, 0, sizeof(unsigned int), g->stream);
-      count_nonfinite<<<4 * prop.multiProcessorCount, 256, 0, g->stream>>>(init, n, flag);
-      cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, g->stream);
-      const cudaError_t e = cudaStreamSynchronize(g->stream);
-      cudaFree(flag);
-      if (e != cudaSuccess) {
-        rc = set_error3(nullptr, SOR_E_CUDA, "non-finite check failed: %s", cudaGetErrorString(e));
-        break;
-      }
-      if (bad) {
-        rc = set_error3(nullptr, SOR_E_INVAL, "init contains non-finite values");
-        break;
-      }
-    }
-    rc = load3d(g, init);
-  } while (0);
-  if (rc < 0) {
-    free3d(g);
-    return rc;
-  }
-  *out = g;
-  return SOR_OK;
-}
-
-int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_change) {
-  if (int rc = usable3(g); rc < 0) return rc;
-  if (!(omega > 0.0 && omega < 2.0)) return set_error3(nullptr, SOR_E_INVAL, "omega must satisfy 0 < omega < 2");
-  if (iters < 0) return set_error3(nullptr, SOR_E_INVAL, "iters must be >= 0");
-  bool conv = false;
-  if (g->dt == SOR_F64)
-    return run3d<double>(g, omega, 0, iters, 1.0, 1, last_max_change != nullptr, nullptr, last_max_change, &conv);
-  return run3d<float>(g, omega, 0, iters, 1.0, 1, last_max_change != nullptr, nullptr, last_max_change, &conv);
-}
-
-int sor3d_solve(sor3d_grid* g, double omega, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
-                double* max_change_out) {
-  if (int rc = usable3(g); rc < 0) return rc;
-  if (!(omega > 0.0 && omega < 2.0)) return set_error3(nullptr, SOR_E_INVAL, "omega must satisfy 0 < omega < 2");
-  if (!(tol > 0.0) || !std::isfinite(tol)) return set_error3(nullptr, SOR_E_INVAL, "tol must be finite and > 0");
-  if (maxit < 1 || check_every < 1 || check_every > maxit)
-    return set_error3(nullptr, SOR_E_INVAL, "need maxit >= 1 and 1 <= check_every <= maxit");
-  bool conv = false;
-  const int rc = g->dt == SOR_F64
-                     ? run3d<double>(g, omega, 1, maxit, tol, check_every, false, iters_out, max_change_out, &conv)
-                     : run3d<float>(g, omega, 1, maxit, tol, check_every, false, iters_out, max_change_out, &conv);
-  if (rc < 0) return rc;
-  return conv ? SOR_OK : SOR_NOT_CONVERGED;
-}
-
-int sor3d_download(sor3d_grid* g, double* out) {
-  if (int rc = usable3(g); rc < 0) return rc;
-  if (!out) return set_error3(nullptr, SOR_E_INVAL, "out is NULL");
-  const int64_t w = g->nx + 2, nrow = (g->nz + 2) * (g->ny + 2);
-  if (g->dt == SOR_F64) {
-    CU3(cudaMemcpy2DAsync(out, w * 8, g->plane, g->pitch * 8, w * 8, nrow, cudaMemcpyDefault, g->stream));
-  } else {
-    dim3 grid((unsigned)std::min<int64_t>((w + 255) / 256, 1024), (unsigned)std::min<int64_t>(nrow, 65535));
-    widen_rows<<<grid, 256, 0, g->stream>>>((const float*)g->plane, g->pitch, g->scratch, w, nrow, w);
-    CU3(cudaGetLastError());
-    CU3(cudaMemcpyAsync(out, g->scratch, (size_t)nrow * w * 8, cudaMemcpyDefault, g->stream));
-  }
-  CU3(cudaStreamSynchronize(g->stream));
-  return SOR_OK;
-}
-
-int sor3d_set_kernel(sor3d_grid* g, int kernel) {
-  if (int rc = usable3(g); rc < 0) return rc;
-  if (kernel != SOR_KERNEL_NATURAL && kernel != SOR_KERNEL_FUSED)
-    return set_error3(nullptr, SOR_E_INVAL, "3-D kernels: SOR_KERNEL_NATURAL or SOR_KERNEL_FUSED");
-  g->kernel = kernel;
-  return SOR_OK;
-}
-
-int sor3d_last_elapsed_ms(const sor3d_grid* g, double* ms) {
-  if (!g || !ms) return set_error3(nullptr, SOR_E_INVAL, "NULL argument");
-  if (!g->have_elapsed) return set_error3(nullptr, SOR_E_STATE, "no iterate/solve call timed yet");
-  *ms = g->elapsed_ms;
-  return SOR_OK;
-}
-
-void sor3d_destroy(sor3d_grid* g) {
-  if (!g) return;
-  if (g->stream) cudaStreamSynchronize(g->stream);
-  free3d(g);
 }
 
 }  // extern "C"

@@ -56,6 +56,27 @@ struct DevState {
   long long conv_iter;
   long long checks;
   double max_change;           // last checked max-change
+  int halo_timeout;            // a halo wait gave up (dist: a peer never released its rows)
+};
+
+// ---------------------------------------------------------------- multi-GPU
+// Per-rank communication block (device memory, mapped by the other ranks of a
+// dist handle over CUDA IPC; SURVEY 8(e) path B).  `done`/`pub` join the
+// per-rank max-changes of a checked pass (E2): a rank publishes its local
+// maxima of pass `seq` in pub[seq & 1] and then releases done = seq; every
+// rank reads all ranks' pub once their done >= seq.  The halo flags follow the
+// header in the same allocation: top[nflags] (released by rank-1 after it
+// pushed its last rows into this rank's top halo) and bot[nflags] (rank+1).
+constexpr int kMaxRanks = 8;  // one NVSwitch node
+struct DistComm {
+  unsigned long long done;
+  unsigned long long pad0[15];
+  unsigned long long pub[2][kMaxT];
+  unsigned long long pad1[16 - (2 * kMaxT) % 16];
+};
+struct DistJoinTab {           // device-resident: every rank's comm block, mapped
+  DistComm* comm[kMaxRanks];
+  int nranks, rank;
 };
 
 // Loop control of one launch (a pass of `T` iterations ending at k_last).
@@ -84,6 +105,14 @@ struct IterCtl {
   int prev_valid;
   int prev_T, prev_ck, prev_set;
   long long prev_k_last;
+  // Cross-rank join of the maxima (dist over IPC): 0 none (one DevState sees
+  // every slab), 1 publish + wait + combine (concurrent ranks), 2 publish
+  // only, 3 combine only (lockstep ranks sharing a GPU: a host barrier runs
+  // between 2 and 3, so no kernel ever waits on another process).
+  const DistJoinTab* join;
+  int join_mode;
+  unsigned long long seq;       // this pass's sequence number (halo flags, join)
+  unsigned long long prev_seq;  // sequence number of the pass the decision block decides
 };
 
 __host__ __device__ __forceinline__ int floordiv6(int x) { return x >= 0 ? x / 6 : -((5 - x) / 6); }
@@ -146,8 +175,62 @@ __device__ __forceinline__ int ld_stop(const DevState* st) {
 // Stop test of Algorithm 1 [P:319-331] for the iterations of one pass (T
 // iterations ending at k_last, max-change mode ck); their maxima are complete
 // in st->maxbits[set].  Strict '<' (reading #7).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin (one thread) until *p >= v; gives up after ~8 s and reports it (a peer
+// that never releases must not hang the GPU).
+__device__ __forceinline__ bool wait_geq_sys(const unsigned long long* p, unsigned long long v, DevState* st) {
+  if (ld_acquire_sys(p) >= v) return true;
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(100);
+    if (globaltimer_ns() - t0 > 8000000000ull) {
+      if (st) atomicExch(&st->halo_timeout, 1);
+      return false;
+    }
+  }
+  return true;
+}
+
+// E2 over IPC: publish this rank's maxima of pass `seq` (slot set `set`) and/or
+// fold every rank's published maxima into them (join_mode, see IterCtl).
+__device__ __forceinline__ void join_maxima(DevState* st, const IterCtl& ctl, int set, unsigned long long seq) {
+  if (!ctl.join || ctl.join_mode == 0) return;
+  const DistJoinTab& J = *ctl.join;
+  DistComm* mine = J.comm[J.rank];
+  if (ctl.join_mode == 1 || ctl.join_mode == 2) {
+    for (int t = 0; t < kMaxT; ++t) mine->pub[seq & 1][t] = st->maxbits[set][t][0];
+    __threadfence_system();
+    st_release_sys(&mine->done, seq);
+  }
+  if (ctl.join_mode == 1 || ctl.join_mode == 3) {
+    for (int q = 0; q < J.nranks; ++q) {
+      if (q == J.rank) continue;
+      DistComm* c = J.comm[q];
+      wait_geq_sys(&c->done, seq, st);
+      for (int t = 0; t < kMaxT; ++t) {
+        const unsigned long long v = *reinterpret_cast<volatile unsigned long long*>(&c->pub[seq & 1][t]);
+        if (v > st->maxbits[set][t][0]) st->maxbits[set][t][0] = v;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl, long long k_last, int T, int ck,
-                                              int set) {
+                                              int set, unsigned long long seq) {
+  join_maxima(st, ctl, set, seq);
+  if (ctl.join_mode == 2) return;  // lockstep: the decision runs after the host barrier
   const long long k0 = k_last - (T - 1);
   st->ticket = 0u;
   for (int t = 0; t < T; ++t) {
@@ -205,7 +288,7 @@ __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl, 
   __threadfence();
 }
 __device__ __forceinline__ void finalize_pass(DevState* st, const IterCtl& ctl) {
-  finalize_pass(st, ctl, ctl.k_last, ctl.T, ctl.ck, ctl.set);
+  finalize_pass(st, ctl, ctl.k_last, ctl.T, ctl.ck, ctl.set, ctl.seq);
 }
 
 // One part (warp or CTA) contributes its maxima; the last part finalizes.
@@ -223,7 +306,7 @@ __device__ __forceinline__ void maybe_finalize(const IterCtl& ctl) {
   }
 }
 
-__global__ void finalize_kernel(IterCtl ctl) {
+static __global__ void finalize_kernel(IterCtl ctl) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     if (ctl.solve && ld_stop(ctl.st)) return;
     finalize_pass(ctl.st, ctl);
@@ -275,6 +358,68 @@ struct WaveMaps {
   CUtensorMap m[2];
 };
 
+// Device-initiated halo exchange (SURVEY 8(e) path B): the tiles that finish
+// a slab's first / last H owned rows also store them into the neighbouring
+// slab's destination plane (a CUDA-IPC mapping of another GPU's memory, or
+// another slab of a virtual grid) and then release that neighbour's flag of
+// their strip with this pass's sequence number.  The tiles whose results
+// depend on halo rows wait for the flags of every producer strip whose tile
+// reads or writes their columns (RAW for the halo, WAR for the plane they
+// are about to push into), so interior tiles never wait and no global
+// barrier or copy kernel separates two passes.
+struct HaloLink {
+  long long up_off, dn_off;       // elements from this slab's dst cell to the same cell in the
+                                  // upper / lower neighbour's dst plane
+  unsigned long long* rel_up;     // upper neighbour's bottom-halo flags (indexed by our strip)
+  unsigned long long* rel_dn;     // lower neighbour's top-halo flags
+  const unsigned long long* acq_top;  // our top-halo flags (released by the upper neighbour)
+  const unsigned long long* acq_bot;  // our bottom-halo flags
+  unsigned long long seq;         // released value (this pass)
+  unsigned long long need;        // wait until flags >= need
+  int H;                          // rows pushed per side (>= the halo any pass reads)
+  int pg, pw, pgh, pn;            // producer strip layout of the awaited pass: strip s owns
+                                  // [pg + s*pw, pg + (s+1)*pw), reads pgh columns more per side;
+                                  // pn strips
+  int on;                         // 0: no link (single slab / host-side exchange)
+};
+
+__host__ __device__ __forceinline__ int floordiv_i(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Lane 0 of the tile's streaming warp: wait for the producer strips whose
+// tiles touch columns [c_a, c_b) (their owned range widened by pgh).
+__device__ __forceinline__ void halo_wait(const unsigned long long* flags, const HaloLink& L, int c_a, int c_b,
+                                          DevState* st) {
+  const int s_a = max(0, floordiv_i(c_a - L.pgh - L.pg, L.pw));
+  const int s_b = min(L.pn - 1, floordiv_i(c_b + L.pgh - 1 - L.pg, L.pw));
+  for (int s = s_a; s <= s_b; ++s)
+    if (!wait_geq_sys(flags + s, L.need, st)) return;
+}
+
+// The storing warp of a tile, after the tile: copy its owned cells of rows
+// [max(R0, lo), min(R1, hi)) from the local dst plane (written by this same
+// lane, so program order makes them visible) to the neighbour, then release.
+template <typename R, int NC>
+__device__ __forceinline__ void halo_push_rows(R* dst, long long g0, long long pitch, long long off, int c0,
+                                               int own_lo, int own_hi, int ra, int rb, int lane,
+                                               unsigned long long* flag, unsigned long long seq) {
+  for (int r = ra; r < rb; ++r) {
+    const R* src = dst + (long long)(r - g0) * pitch + c0;
+#pragma unroll
+    for (int h = 0; h < NC / 2; ++h) {
+      const int cp = c0 + 2 * h;
+      if (cp >= own_lo && cp + 1 < own_hi) {
+        const R x = src[2 * h], y = src[2 * h + 1];
+        R* q = dst + (long long)(r - g0) * pitch + c0 + off + 2 * h;
+        q[0] = x;
+        q[1] = y;
+      }
+    }
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) st_release_sys(flag, seq);
+}
+
 template <typename R>
 struct WaveArgs {
   const R* src;      // column 0 of storage row 0 (plane + kColPad)
@@ -287,7 +432,46 @@ struct WaveArgs {
   int ntiles;
   int s0;            // first column of strip 0 (multiple of 4)
   R w;
+  HaloLink link;     // device-initiated halo exchange (multi-slab)
 };
+
+// A tile whose owned rows lie within `need_rows` of the slab edge depends on
+// the halo: its streaming warp waits before the first TMA of source rows.
+template <typename R>
+__device__ __forceinline__ void tile_halo_wait(const WaveArgs<R>& a, int sw, int wc, int R0, int R1, int need_rows,
+                                               int lane, DevState* st) {
+  const HaloLink& L = a.link;
+  if (!L.on) return;
+  const bool top = L.acq_top != nullptr && R0 < a.r_lo + need_rows;
+  const bool bot = L.acq_bot != nullptr && R1 > a.r_hi - need_rows;
+  if (!(top || bot)) return;
+  if (lane == 0) {
+    if (top) halo_wait(L.acq_top, L, sw, sw + wc, st);
+    if (bot) halo_wait(L.acq_bot, L, sw, sw + wc, st);
+    // the rows were written through the generic proxy (peer stores); the
+    // tile reads them with TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+}
+// The storing warp of a tile that finished rows within H of the slab edge
+// pushes them (its owned columns: the strip minus `ghost` per side).  The
+// tiler gives every strip exactly one such tile per side (sor_api.cu).
+template <typename R, int NC>
+__device__ __forceinline__ void tile_halo_push(const WaveArgs<R>& a, int sw, int wc, int ghost, int strip, int R0,
+                                               int R1, int lane) {
+  const HaloLink& L = a.link;
+  if (!L.on) return;
+  const int c0 = sw + NC * lane;
+  const int own_lo = sw + ghost, own_hi = sw + wc - ghost;
+  const int lo = (int)a.r_lo, hi = (int)a.r_hi;
+  if (L.rel_up != nullptr && R0 < lo + L.H)
+    halo_push_rows<R, NC>(a.dst, a.g0, a.pitch, L.up_off, c0, own_lo, own_hi, R0, min(R1, lo + L.H), lane,
+                          L.rel_up + strip, L.seq);
+  if (L.rel_dn != nullptr && R1 > hi - L.H)
+    halo_push_rows<R, NC>(a.dst, a.g0, a.pitch, L.dn_off, c0, own_lo, own_hi, max(R0, hi - L.H), R1, lane,
+                          L.rel_dn + strip, L.seq);
+}
 
 __device__ __forceinline__ void ldg4(const double* p, double (&x)[4]) {
   asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -933,7 +1117,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
   if (ctl.st && ctl.solve) {
     if (ctl.defer && blockIdx.x == 0) {  // the decision block: stop test of the previous pass
       if (threadIdx.x == 0 && ctl.prev_valid && !ld_stop(ctl.st))
-        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set);
+        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set, ctl.prev_seq);
       return;
     }
     // one read per CTA: with a deferred stop test the flag can change while
@@ -943,7 +1127,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     __syncthreads();
     if (cta_stop) return;
   }
-  unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
+  unsigned long long dm[kMaxT] = {};
   if (has_tile) {
     const int sw = a.s0 + tile.x * (WC - 4 * T);
     const int R0 = tile.y;
@@ -952,6 +1136,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     // i_first even; nsteps a multiple of 6 (ring phase x parity)
     const int i_first = (R0 - (2 * T - 1)) & ~1;
     const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
+    if (role == 0) tile_halo_wait(a, sw, WC, R0, R1, 2 * T, lane, ctl.st);
     if (SPLIT) {
       unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST, NC>();
       R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST, NC>());
@@ -964,6 +1149,14 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     } else {
       unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
       wave_tile<R, T, NST, CK, 0, 2 * T, NC>(a, tm.m, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+    }
+  }
+  if (a.link.on && (!SPLIT || (threadIdx.x >> 5) & 1)) {
+    // re-read the tile (nothing of it stays live across the stream loop)
+    const int gw2 = ((int)blockIdx.x - ctl.defer) * wave_tiles_per_cta(SPLIT) + (SPLIT ? (int)(threadIdx.x >> 6) : (int)(threadIdx.x >> 5));
+    if ((int)blockIdx.x >= ctl.defer && gw2 < a.ntiles) {
+      const int4 t2 = a.tiles[gw2];
+      tile_halo_push<R, NC>(a, a.s0 + t2.x * (WC - 4 * T), WC, 2 * T, t2.x, t2.y, t2.z, (int)(threadIdx.x & 31));
     }
   }
   (void)role;
@@ -1134,7 +1327,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
   if (ctl.st && ctl.solve) {
     if (ctl.defer && blockIdx.x == 0) {  // the decision block (see wave_kernel)
       if (threadIdx.x == 0 && ctl.prev_valid && !ld_stop(ctl.st))
-        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set);
+        finalize_pass(ctl.st, ctl, ctl.prev_k_last, ctl.prev_T, ctl.prev_ck, ctl.prev_set, ctl.prev_seq);
       return;
     }
     __shared__ int cta_stop;
@@ -1148,13 +1341,14 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gw = ((int)blockIdx.x - ctl.defer) * kWaveWarps + warp;
-  unsigned long long dm[kMaxT] = {0ull, 0ull, 0ull, 0ull};
+  unsigned long long dm[kMaxT] = {};
   if (gw < a.ntiles) {
     const int4 tile = a.tiles[gw];
     const int sw = a.s0 + tile.x * (WC - 2 * G);
     const int R0 = tile.y, R1 = tile.z;
     const int i_first = (R0 - (T - 1)) & ~1;
     const int nsteps = (R1 + T - 1 - i_first + 5) / 6 * 6;
+    tile_halo_wait(a, sw, WC, R0, R1, T, lane, ctl.st);
     unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
     Pipe P;
 #pragma unroll
@@ -1212,6 +1406,13 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
     P.run(a, i_first);
 #pragma unroll
     for (int t = 0; t < Pipe::NSLOT; ++t) dm[t] = P.dmax[t];
+  }
+  if (a.link.on) {
+    const int gw2 = ((int)blockIdx.x - ctl.defer) * kWaveWarps + (int)(threadIdx.x >> 5);
+    if ((int)blockIdx.x >= ctl.defer && gw2 < a.ntiles) {
+      const int4 t2 = a.tiles[gw2];
+      tile_halo_push<R, NC>(a, a.s0 + t2.x * (WC - 2 * G), WC, G, t2.x, t2.y, t2.z, (int)(threadIdx.x & 31));
+    }
   }
   if (CK != 0) {
     constexpr int NS = CK == 2 ? T : 1;
@@ -1482,14 +1683,14 @@ __global__ void __launch_bounds__(1024) k5_small_solve(R* base, long long pitch,
 
 // ---------------------------------------------------------------- layout
 // fp64 -> fp32 round-to-nearest (reading #17) and exact widening, row blocks.
-__global__ void narrow_rows(const double* __restrict__ src, long long src_ld, float* dst,
+static __global__ void narrow_rows(const double* __restrict__ src, long long src_ld, float* dst,
                             long long dst_ld, long long nrows, long long ncols) {
   for (long long r = blockIdx.y; r < nrows; r += gridDim.y)
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncols;
          c += (long long)gridDim.x * blockDim.x)
       dst[r * dst_ld + c] = __double2float_rn(src[r * src_ld + c]);
 }
-__global__ void widen_rows(const float* __restrict__ src, long long src_ld, double* dst,
+static __global__ void widen_rows(const float* __restrict__ src, long long src_ld, double* dst,
                            long long dst_ld, long long nrows, long long ncols) {
   for (long long r = blockIdx.y; r < nrows; r += gridDim.y)
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncols;
@@ -1497,7 +1698,7 @@ __global__ void widen_rows(const float* __restrict__ src, long long src_ld, doub
       dst[r * dst_ld + c] = (double)src[r * src_ld + c];
 }
 // Non-finite detector for sor_create's validation of device-resident input.
-__global__ void count_nonfinite(const double* __restrict__ p, long long n, unsigned int* out) {
+static __global__ void count_nonfinite(const double* __restrict__ p, long long n, unsigned int* out) {
   unsigned int bad = 0;
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < n;
        c += (long long)gridDim.x * blockDim.x)

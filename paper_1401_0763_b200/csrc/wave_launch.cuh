@@ -1,0 +1,121 @@
+// wave_launch.cuh — launchers of the wave (K3/K4) and Jacobi kernels, one
+// explicit instantiation per (dtype, depth) translation unit (wave_*.cu,
+// jacobi_inst.cu) so the library builds in parallel.
+#pragma once
+
+#include "sor_internal.h"
+
+namespace sorh {
+
+template <typename R>
+constexpr int wave_nst() { return 14; }
+
+template <typename R, int T, int CK, bool SPLIT, int NC>
+int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  constexpr int NST = wave_nst<R>();
+  constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
+  constexpr int per_cta = wave_tiles_per_cta(SPLIT);
+  static int occ_dev[kMaxDev] = {};  // resident CTAs/SM for this instance, per device
+  int& occ = occ_dev[g->device % kMaxDev];
+  if (occ == 0) {
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT, NC>, kWaveWarps * 32, smem);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[g->cur]);
+  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = w;
+  a.s0 = -4 * ((2 * T + 3) / 4);
+  const int slab_idx = (int)(&s - &g->slabs[0]);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  a.link = make_link(g, s, g->cur, g->nxt(g->cur));
+  record_layout(g, g->nxt(g->cur), a.s0, wave_cols<NC>(), 2 * T, strips_of(g, a.s0, wave_cols<NC>(), 2 * T));
+  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta) + (ctl.defer ? 1 : 0);
+  IterCtl c = ctl;
+  c.finalize = fused_fin ? 1 : 0;
+  c.nparts = blocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // PDL only for one-wave launches (wave_pdl)
+  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC>, a, c, s.tmap[g->cur]));
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+template <typename R, int T, int CK>
+int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  // 4 columns per lane: wider lanes (NC = 6, 8; bitwise equal) measured
+  // slower on B200 at every T (fewer resident warps outweigh the extra ILP).
+  // T >= 2: warp pairs (split).
+  return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
+}
+
+// Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
+template <typename R, int T, int CK>
+int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {
+  constexpr int NST = wave_nst<R>();
+  constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST, kWaveNC>();
+  constexpr int G = jacobi_ghost(T);
+  static int occ_dev[kMaxDev] = {};
+  int& occ = occ_dev[g->device % kMaxDev];
+  if (occ == 0) {
+    CU(cudaFuncSetAttribute(jacobi_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[g->cur]);
+  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = R(1);
+  a.s0 = -4 * ((G + 3) / 4);
+  const int slab_idx = (int)(&s - &g->slabs[0]);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, slab_idx, G, T, wave_cols<kWaveNC>(), occ * kWaveWarps, false, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  a.link = make_link(g, s, g->cur, g->nxt(g->cur));
+  record_layout(g, g->nxt(g->cur), a.s0, wave_cols<kWaveNC>(), G, strips_of(g, a.s0, wave_cols<kWaveNC>(), G));
+  const unsigned blocks = (unsigned)((a.ntiles + kWaveWarps - 1) / kWaveWarps) + (ctl.defer ? 1 : 0);
+  IterCtl c = ctl;
+  c.finalize = fused_fin ? 1 : 0;
+  c.nparts = blocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK>, a, c, s.tmap[g->cur]));
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+}  // namespace sorh
