@@ -112,56 +112,118 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The reference arm for this tier: the CPU oracle as it stands (no
+    reference implementation exists), on the same fixed window as our arm's
+    cpu_baseline; each step = the window at all cores, after the thread-scaling
+    sweep (reported, not timed into `value`)."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
     import oracle
     cfg = SI.config(args.config, dtype=args.dtype)
     cores = len(os.sched_getaffinity(0))
+    window = args.cpu_window
     init = cfg.init()
-    u = oracle.to_storage(init, cfg.dtype)
-    # bounded sample per step: `sample_iters` iterations of the workload grid
-    sample_iters = args.ref_iters
     for _ in range(args.warmup):
+        u = oracle.to_storage(init, cfg.dtype)
         oracle.iterate(u, cfg.omega, 1, threads=cores)
     ts = []
     for _ in range(args.steps):
+        u = oracle.to_storage(init, cfg.dtype)
         t0 = time.perf_counter()
-        oracle.iterate(u, cfg.omega, sample_iters, threads=cores)
+        oracle.iterate(u, cfg.omega, window, threads=cores)
         ts.append(time.perf_counter() - t0)
     t = sum(ts)
-    glups = cfg.rows * cfg.cols * sample_iters * args.steps / t / 1e9
+    glups = cfg.rows * cfg.cols * window * args.steps / t / 1e9
+    scaling = cpu_protocol(cfg, window, thread_counts(cores)) if args.steps > 0 else {}
     line = {
         "impl": "reference", "metric": "GLUP/s", "value": glups, "unit": "GLUP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic",
-        "config": {"workload": f"{cfg.name} sample: {sample_iters} iterations of the {cfg.rows}x{cfg.cols} "
-                               f"{cfg.dtype} grid per step", "impl": "CPU oracle (oracle/sor_oracle.c, "
-                               "pthreads row slabs + barrier per phase, bitwise = serial oracle)"},
+        "config": {"workload": f"{cfg.name} window: iterations 1..{window} of the {cfg.rows}x{cfg.cols} "
+                               f"{cfg.dtype} grid from its initial state, per step", "impl": "CPU oracle "
+                               "(oracle/sor_oracle.c, pthreads row slabs + barrier per phase, bitwise = serial oracle)"},
         "cpu_baseline": {"value": glups, "unit": "GLUP/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{sample_iters} iterations of {cfg.name} per step, {args.steps} steps"},
+                         "sample": f"iterations 1..{window} of {cfg.name} per step, {args.steps} steps, all cores",
+                         "threads": {k: round(v, 4) for k, v in scaling.items()}, "host": host_info()},
         "e2e": {"value": glups, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline(cfg, budget_s: float):
-    """Oracle (as it stands) on this host's cores, bounded to ~budget_s seconds."""
+def host_info():
+    """CPU model, sockets / NUMA nodes, host RAM (the CPU baseline's hardware)."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                if ln.startswith("physical id"):
+                    sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 2 ** 20, 1)
+    except OSError:
+        pass
+    numa = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")]) \
+        if os.path.isdir("/sys/devices/system/node") else None
+    return {"cpu_model": model, "sockets": len(sockets) or None, "numa_nodes": numa, "ram_gib": ram,
+            "cores_available": len(os.sched_getaffinity(0))}
+
+
+def thread_counts(cores):
+    return sorted({t for t in (1, 2, 4, 8, cores) if t <= cores})
+
+
+def cpu_protocol_child(cfg_name, dtype, window, threads):
+    """The CPU-baseline protocol (the paper's thread scaling
+    P:383-389): the oracle as it stands, on a fixed window -- iterations
+    1..window of the workload from its initial grid -- once per thread count,
+    one oracle call per window (threads spawned once).  Run in a clean child
+    process, so nothing of the GPU process (driver threads, pinned buffers)
+    shares the cores or the memory with it."""
     import oracle
+    cfg = SI.config(cfg_name, dtype=dtype)
+    init = cfg.init()
+    out = {}
+    for P in threads:
+        u = oracle.to_storage(init, cfg.dtype)
+        t0 = time.perf_counter()
+        oracle.iterate(u, cfg.omega, window, threads=P)
+        dt = time.perf_counter() - t0
+        out[str(P)] = cfg.rows * cfg.cols * window / dt / 1e9
+    return out
+
+
+def cpu_protocol(cfg, window, threads):
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-protocol-child", "--config", cfg.name,
+           "--dtype", cfg.dtype, "--cpu-window", str(window), "--cpu-threads", ",".join(map(str, threads))]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    if r.returncode != 0:
+        raise RuntimeError("cpu protocol child failed: " + r.stderr[-2000:])
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(cfg, window):
+    """Oracle (as it stands) on this host's cores: the fixed-window protocol
+    at 1/2/4/8/all threads; `value` is the all-cores rate."""
     cores = len(os.sched_getaffinity(0))
-    u = oracle.to_storage(cfg.init(), cfg.dtype)
-    n = 0
-    t0 = time.perf_counter()
-    chunk = 2
-    while time.perf_counter() - t0 < budget_s:
-        oracle.iterate(u, cfg.omega, chunk, threads=cores)
-        n += chunk
-    t = time.perf_counter() - t0
-    return {"value": cfg.rows * cfg.cols * n / t / 1e9, "unit": "GLUP/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {n} iterations of {cfg.name} ({cfg.rows}x{cfg.cols} {cfg.dtype}), "
-                      f"threaded oracle, {t:.1f} s"}
+    ths = thread_counts(cores)
+    rates = cpu_protocol(cfg, window, ths)
+    return {"value": rates[str(cores)], "unit": "GLUP/s", "cores": cores, "kind": "oracle",
+            "sample": (f"iterations 1..{window} of {cfg.name} ({cfg.rows}x{cfg.cols} {cfg.dtype}) from its "
+                       f"initial grid, threaded oracle (P workers + barrier per phase), one call per thread "
+                       f"count, clean child process"),
+            "threads": {k: round(v, 4) for k, v in rates.items()},
+            "host": host_info()}
 
 
 # ------------------------------------------------------------------ NEXT rows
@@ -264,6 +326,87 @@ def run_next(args):
     return 0
 
 
+# ------------------------------------------------------------------ multi-GPU / C5
+def ipc_self_check(P, SI, make_grid, rank):
+    """IPC vs NCCL on this node: 61 iterations + a short solve of a 1024^2
+    grid with random interior, grids compared bitwise on rank 0."""
+    import torch
+    import torch.distributed as dist
+    try:
+        cfg = SI.config("C2")
+        init = SI.random_field(cfg.rows, cfg.cols, seed=3, lo=-10.0, hi=10.0)
+        dinit = torch.from_numpy(init).cuda()
+        res = {}
+        for tr in ("nccl", "ipc"):
+            g = make_grid(cfg, dinit, tr)
+            g.set_kernel("temporal", 4)
+            g.iterate(1.9, 61)
+            r = g.solve(1.9, 1e-3, 4000, 1)
+            out = g.download()
+            res[tr] = (out, r.iters, r.max_change)
+            g.close()
+        ok = 1
+        if rank == 0:
+            a, b = res["nccl"], res["ipc"]
+            ok = int(np.array_equal(a[0], b[0]) and a[1:] == b[1:])
+        f = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.broadcast(f, 0)
+        return {"ok": bool(f.item()), "what": "iterate 61 + solve(1e-3) of a 1024^2 random field, T=4, "
+                "IPC vs NCCL, bitwise"}
+    except Exception as e:  # noqa: BLE001
+        return {"ok": False, "error": str(e)[:300]}
+
+
+def measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, pk, pk_kind, reps=3):
+    """C5 (BJ configs[4]) at N GPUs: reset from the HBM-resident init, then
+    iterate(omega_opt, 200) at T=4; device time, max over ranks."""
+    cfg = SI.config("C5")
+    init_h = cfg.init()
+    init_d = torch.from_numpy(init_h).cuda() if (world == 1 or rank == 0) else None
+    del init_h
+    g = make_grid(cfg, init_d, transport)
+    g.set_kernel("temporal", 4)
+    g.iterate(cfg.omega, cfg.iters)            # warm-up (tile tables, tensor maps)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ts, launches = [], 0
+    for _ in range(reps):
+        g.reset(init_d if (world == 1 or rank == 0) else None)
+        if world > 1:
+            dist.barrier()
+        g.iterate(cfg.omega, cfg.iters)
+        ms = g.elapsed_ms
+        if world > 1:
+            tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        ts.append(ms)
+        launches += g.stats["kernel_launches"]
+    ck = clocks.stop()
+    rows_local = g.stats["row_hi"] - g.stats["row_lo"]
+    g.close()
+    ms = float(np.median(ts))
+    value = cfg.rows * cfg.cols * cfg.iters / (ms * 1e-3) / 1e9
+    t_launch = ms / (launches / reps)
+    bpl = 16 * rows_local * cfg.cols
+    achieved = bpl / (t_launch * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            tr = json.load(f)
+        traffic = tr.get("C5:wave_kernel<f64,T=4,ck=0>", {}).get("dram_bytes_per_launch")
+    return {"metric": "GLUP/s", "value": value, "unit": "GLUP/s", "ms": ms, "reps_ms": ts,
+            "workload": f"C5: {cfg.rows}x{cfg.cols} f64, random edges seed 7, omega={cfg.omega!r}, "
+                        f"{cfg.iters} iterations, T=4, median of {reps}",
+            "n_gpus": world, "scaling": "strong",
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                         "kernel": "wave_kernel<f64,T=4,ck=0>", "algorithmic_bytes_per_launch": bpl,
+                         "avg_launch_ms": t_launch, "peak_kind": pk_kind},
+            "clocks": ck}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -276,14 +419,25 @@ def main():
     ap.add_argument("--kernel", default="temporal")
     ap.add_argument("--T", type=int, default=4)
     ap.add_argument("--no-solve", action="store_true", help="fixed iterations only")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--ref-iters", type=int, default=32)
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="NEXT rows: single-thread oracle budget (s)")
+    ap.add_argument("--cpu-window", type=int, default=96,
+                    help="CPU baseline / reference arm: iterations 1..W of the workload")
+    ap.add_argument("--cpu-threads", default=None)
+    ap.add_argument("--cpu-protocol-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1: halo/max transport (ipc: device-initiated pushes over CUDA IPC)")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (32768^2) sub-record")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--method", default="sor", choices=["sor", "jacobi", "sor3d"],
                     help="sor: the headline path; jacobi / sor3d: the NEXT-2 / NEXT-3 rows (1 GPU)")
     args = ap.parse_args()
     if args.dtype is None:
         args.dtype = "f32" if args.config == "C4F32" else "f64"
+    if args.cpu_protocol_child:
+        rates = cpu_protocol_child(args.config, args.dtype, args.cpu_window,
+                                   [int(x) for x in args.cpu_threads.split(",")])
+        print(json.dumps(rates), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     if args.method != "sor":
@@ -305,14 +459,31 @@ def main():
     init_h = cfg.init()
     init_d = torch.from_numpy(init_h).cuda()
 
-    if world > 1:
-        uid = P.nccl_unique_id() if rank == 0 else bytes(128)
-        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).cuda()
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().numpy().tobytes())
-        g = P.Grid.create_dist(init_d, rank, world, local, uid, dtype=cfg.dtype)
-    else:
-        g = P.Grid.create(init_d, dtype=cfg.dtype)
+    def bcast_id(make):
+        uid = make() if rank == 0 else bytes(128)
+        tb = torch.frombuffer(bytearray(uid), dtype=torch.uint8).cuda()
+        dist.broadcast(tb, 0)
+        return bytes(tb.cpu().numpy().tobytes())
+
+    def make_grid(c, dinit, transport):
+        """One handle of config c: single GPU, or row slabs over `transport`."""
+        if world == 1:
+            return P.Grid.create(dinit, dtype=c.dtype)
+        if transport == "ipc":
+            return P.Grid.create_dist_ipc(dinit if rank == 0 else None, rank, world, local,
+                                          bcast_id(P.ipc_unique_id), dtype=c.dtype, rows=c.rows, cols=c.cols)
+        return P.Grid.create_dist(dinit if rank == 0 else None, rank, world, local, bcast_id(P.nccl_unique_id),
+                                  dtype=c.dtype, rows=c.rows, cols=c.cols)
+
+    transport, transport_check = args.transport, None
+    if world > 1 and transport == "ipc":
+        # the device-initiated path is checked against the NCCL path on this
+        # node before it is timed (a short iterate + solve, bitwise); any
+        # mismatch or error falls back to NCCL and says so in the JSON line
+        transport_check = ipc_self_check(P, SI, make_grid, rank)
+        if not transport_check.get("ok"):
+            transport = "nccl"
+    g = make_grid(cfg, init_d, transport)
     g.set_kernel(args.kernel, args.T if args.kernel == "temporal" else 1)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -416,7 +587,8 @@ def main():
             "iterations_per_step": iters_total / len(recs),
             "solve_iterations": recs[-1]["solve_iters"],
             "l2": "flushed between steps (256 MiB write); grid planes 2x134 MB exceed the 126 MB L2",
-            "parallelism": f"row-slab x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"row slabs x{world}, halos and max join over {transport}"
+                            if world > 1 else "single GPU"),
         },
         "fixed_phase_glups": it_glups,
         "solve_phase_glups": sv_glups,
@@ -451,9 +623,16 @@ def main():
         nbytes = hin.numel() * 8
         line["e2e"] = {"value": cfg.rows * cfg.cols * e_iters / t / 1e9, "unit": "GLUP/s",
                        "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
-    if rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget)
+    if transport_check is not None:
+        line["transport_check"] = transport_check
     g.close()
+    del g
+    # BJ's metric also names 32768^2: the C5 sub-record (BJ configs[4]:
+    # 32768x32768 f64, omega_opt, 200 iterations, temporally blocked T=4)
+    if not args.no_c5 and args.config == "C3":
+        line["c5"] = measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, pk, pk_kind)
+    if rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_window)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -22,21 +22,24 @@ def _run(args, timeout):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--ref-iters", "2"], 600)
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-window", "2"], 600)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+    cb = d["cpu_baseline"]
+    assert "1" in cb["threads"] and str(cb["cores"]) in cb["threads"] and cb["host"]["cores_available"] >= 1
     assert "workload" in d["config"]
 
 
 @pytest.mark.gpu
 def test_headline_line():
-    d = _run(["--steps", "2", "--warmup", "3", "--cpu-budget", "1"], 900)
+    d = _run(["--steps", "2", "--warmup", "3", "--cpu-window", "4", "--no-c5"], 900)
     assert BASE_KEYS <= set(d) and d["metric"] == "GLUP/s" and d["value"] > 0
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor", "alu") and 0 < r["frac"] and r["peak"] > 0 and r["unit"] == "GB/s"
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"] and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["solve_iterations"] == 12480 and d["config"]["iterations_per_step"] == 13480
+    assert set(d["cpu_baseline"]["threads"]) >= {"1", str(d["cpu_baseline"]["cores"])}
 
 
 @pytest.mark.gpu

@@ -159,3 +159,67 @@ def test_paper_replay(gpu, orc):
         st = g.stats
     assert r.converged and r.iters == 28000 and st["checks"] == 7
     assert r.max_change < 1e-5 and abs(r.max_change * 28000 / c - 1.0) < 2e-3
+
+
+def test_paper_replay_full_size_bitwise(gpu, orc):
+    """NEXT-1 at the paper's own size [P:375, P:383]: 4096 x 4096, north = 1,
+    omega = 0.376, eps = 1e-5, K = 4000 -- the whole grid after the converging
+    iteration, the iteration count and the checked max-change, bitwise against
+    the threaded oracle (== serial oracle, pin P14)."""
+    cfg = SI.config("PAPER")
+    ref = cfg.init()
+    rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, cfg.check_every, threads=THREADS)
+    with gpu.Grid.create(cfg.init()) as g:
+        g.set_kernel("temporal", 4)
+        r = g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every)
+        out = g.download()
+    assert (r.converged, r.iters, r.max_change) == (rr.status == 0, rr.iters, rr.max_change)
+    assert rr.iters == 28000
+    assert np.array_equal(out, ref)
+
+
+_MULTIWAVE = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, sor_inputs as SI, paper_1401_0763_b200 as P
+n = 0
+for (rows, cols) in ((300, 517), (613, 1029)):
+    init = SI.random_field(rows, cols, seed=rows + cols, lo=-30.0, hi=70.0)
+    for dtype in ("f64", "f32"):
+        for T in (1, 2, 3, 4):
+            ref = oracle.to_storage(init, dtype)
+            rep = oracle.iterate(ref, 1.87, 9, measure_last=True)
+            for nslabs in (1, 3):
+                mk = (lambda: P.Grid.create(init, dtype=dtype)) if nslabs == 1 else \
+                     (lambda: P.Grid.create_virtual(init, nslabs, dtype=dtype))
+                with mk() as g:
+                    g.set_kernel("temporal" if T > 1 else "fused", T)
+                    d = g.iterate(1.87, 9, want_delta=True)
+                    out = g.download()
+                assert np.array_equal(out, ref.astype(np.float64)), (rows, cols, dtype, T, nslabs)
+                assert d == rep.max_change, (rows, cols, dtype, T, nslabs)
+                n += 1
+    ref = init.copy(); rr = oracle.solve(ref, 1.9, 1e-5, 20000, 1)
+    with P.Grid.create(init) as g:
+        g.set_kernel("temporal", 4)
+        r = g.solve(1.9, 1e-5, 20000, 1)
+        assert (r.iters, r.max_change) == (rr.iters, rr.max_change) and np.array_equal(g.download(), ref)
+    n += 1
+print("ok", n)
+"""
+
+
+@pytest.mark.parametrize("env", [{"SOR_WAVE_WAVES": "4", "SOR_WAVE_MIN_BAND": "40"},
+                                 {"SOR_WAVE_WAVES": "9", "SOR_WAVE_MIN_BAND": "16"}])
+def test_multiwave_tiler_random_interior(gpu, env):
+    """The multi-wave tiler (the C4/C5 launch path: bands in row-major order,
+    several waves of CTAs) forced on random-interior grids, whole grid bitwise
+    for T = 1..4, both dtypes, one slab and three pushing slabs, plus a solve.
+    Its seams between bands and strips are otherwise only seen on C4/C5
+    patches of mostly-zero grids."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _MULTIWAVE % root], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().startswith("ok"), r.stderr[-3000:]
