@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsor.so")
-OBJDIR = os.path.join(PKG, "build_obj")
+OBJDIR = os.path.join(os.environ.get("SORB_OBJDIR", "/tmp"), "sorb_build_obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1094,25 +1094,37 @@ bool wave_pdl(const sor_grid* g, unsigned blocks, int occ) {
   return !off && (single_part(g) || g->push) && !g->lockstep && blocks <= (unsigned)(occ * g->nsm);
 }
 
+template <typename R, int T, int CK>
+int launch_wave_L(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  return g->push ? launch_wave_T<R, T, CK, true>(g, s, w, ctl, fused_fin)
+                 : launch_wave_T<R, T, CK, false>(g, s, w, ctl, fused_fin);
+}
+
 template <typename R, int CK>
 int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool fused_fin) {
-  if (CK >= 3 && T == 1) return launch_wave_T<R, 1, 2>(g, s, w, ctl, fused_fin);  // unused combination
+  if (CK >= 3 && T == 1) return launch_wave_L<R, 1, 2>(g, s, w, ctl, fused_fin);  // unused combination
   switch (T) {
-    case 1: return launch_wave_T<R, 1, CK>(g, s, w, ctl, fused_fin);
-    case 2: return launch_wave_T<R, 2, CK>(g, s, w, ctl, fused_fin);
-    case 3: return launch_wave_T<R, 3, CK>(g, s, w, ctl, fused_fin);
-    case 4: return launch_wave_T<R, 4, CK>(g, s, w, ctl, fused_fin);
+    case 1: return launch_wave_L<R, 1, CK>(g, s, w, ctl, fused_fin);
+    case 2: return launch_wave_L<R, 2, CK>(g, s, w, ctl, fused_fin);
+    case 3: return launch_wave_L<R, 3, CK>(g, s, w, ctl, fused_fin);
+    case 4: return launch_wave_L<R, 4, CK>(g, s, w, ctl, fused_fin);
   }
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
+}
+
+template <typename R, int T, int CK>
+int launch_jacobi_L(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {
+  return g->push ? launch_jacobi_T<R, T, CK, true>(g, s, ctl, fused_fin)
+                 : launch_jacobi_T<R, T, CK, false>(g, s, ctl, fused_fin);
 }
 
 template <typename R, int CK>
 int launch_jacobi(sor_grid* g, const Slab& s, int T, const IterCtl& ctl, bool fused_fin) {
   switch (T) {
-    case 1: return launch_jacobi_T<R, 1, CK>(g, s, ctl, fused_fin);
-    case 2: return launch_jacobi_T<R, 2, CK>(g, s, ctl, fused_fin);
-    case 3: return launch_jacobi_T<R, 3, CK>(g, s, ctl, fused_fin);
-    case 4: return launch_jacobi_T<R, 4, CK>(g, s, ctl, fused_fin);
+    case 1: return launch_jacobi_L<R, 1, CK>(g, s, ctl, fused_fin);
+    case 2: return launch_jacobi_L<R, 2, CK>(g, s, ctl, fused_fin);
+    case 3: return launch_jacobi_L<R, 3, CK>(g, s, ctl, fused_fin);
+    case 4: return launch_jacobi_L<R, 4, CK>(g, s, ctl, fused_fin);
   }
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
 }

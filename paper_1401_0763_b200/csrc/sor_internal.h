@@ -175,9 +175,9 @@ void record_layout(sor_grid* g, int dst, int s0, int wc, int ghost, int nstrips)
 int strips_of(const sor_grid* g, int s0, int wc, int ghost);
 
 // Launchers (explicitly instantiated in wave_*.cu / jacobi_inst.cu).
-template <typename R, int T, int CK>
+template <typename R, int T, int CK, bool LINK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin);
-template <typename R, int T, int CK>
+template <typename R, int T, int CK, bool LINK>
 int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin);
 
 }  // namespace sorh

@@ -41,6 +41,13 @@ constexpr int kWaveNC = 4;     // columns per lane in wave_kernel (strip = 32*kW
 
 constexpr int kMaxT = 4;      // max temporal depth (iterations per HBM pass)
 
+// Wave-kernel build options (A/B experiments; the defaults are the product):
+// SOR_WAVE_HOIST issues every stage's lane-neighbour shuffle at the start of
+// a step instead of just before the stage.
+#ifndef SOR_WAVE_HOIST
+#define SOR_WAVE_HOIST 0
+#endif
+
 struct DevState {
   // ordered bits of max |delta| per iteration of a pass, in two slot sets
   // (consecutive passes of a deferred solve alternate); one 128-B line each
@@ -798,6 +805,18 @@ struct WavePipe {
       const int lo_s = max(0, i - R1 + 1), hi_s = min(S - 1, i - R0);
       rowm = hi_s >= lo_s ? (((2u << hi_s) - 1u) & ~((1u << lo_s) - 1u)) : 0u;
     }
+#if SOR_WAVE_HOIST
+    // the lane-neighbour values every stage of this step needs were produced
+    // at the previous step: issue all shuffles first, off the stages'
+    // critical path (a shuffle's latency is ~24 cycles on sm_100a)
+    R nbs[SE - SB];
+#pragma unroll
+    for (int s = SB; s < SE; ++s) {
+      const R wl = s == 0 ? F[P2][1 - O + 2 * (NH - 1)] : C[s > 0 ? s - 1 : 0][P1][NH - 1];
+      const R wf = s == 0 ? F[P2][1 - O] : C[s > 0 ? s - 1 : 0][P1][0];
+      nbs[s - SB] = (O == 0) ? shfl_up1(wl) : shfl_dn1(wf);
+    }
+#endif
 #pragma unroll
     for (int s = SB; s < SE; ++s) {
       const int r = i - s;
@@ -825,7 +844,11 @@ struct WavePipe {
       // W/E neighbours of cell q = O+2h are the other colour's h-1, h (O = 0)
       // or h, h+1 (O = 1); the one outside the lane is the left lane's last
       // (O = 0) or the right lane's first (O = 1)
+#if SOR_WAVE_HOIST
+      const R nb = nbs[s - SB];
+#else
       const R nb = (O == 0) ? shfl_up1(w[NH - 1]) : shfl_dn1(w[0]);
+#endif
       R v[NH], pcor[NH];
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
@@ -1081,7 +1104,10 @@ __host__ __device__ constexpr int wave_min_blocks(int T, bool split, int NC) {
 // was measured to be the slower warp at K = T, so it gets fewer stages.
 // (Measured on B200, C3/C5: T = 4 -> K = 3 is 2-4% faster than K = 4, K = 2
 // slower; T = 3 -> K = 3 beats K = 2; T = 2 needs K = 2.)
-__host__ __device__ constexpr int wave_split_stage(int T) { return T == 4 ? 3 : T; }
+#ifndef SOR_WAVE_K4
+#define SOR_WAVE_K4 3
+#endif
+__host__ __device__ constexpr int wave_split_stage(int T) { return T == 4 ? SOR_WAVE_K4 : T; }
 // warps (tiles, or warp pairs in split mode) per CTA
 __host__ __device__ constexpr int wave_tiles_per_cta(bool split) { return split ? kWaveWarps / 2 : kWaveWarps; }
 template <typename R, int NST, bool SPLIT, int NC>
@@ -1089,7 +1115,18 @@ __host__ __device__ constexpr int wave_smem_bytes() {
   return SPLIT ? (kWaveWarps / 2) * wave_smem_per_pair<R, NST, NC>() : kWaveWarps * wave_smem_per_warp<R, NST, NC>();
 }
 
-template <typename R, int T, int NST, int CK, bool SPLIT, int NC>
+// Warp pairs: the front warp (stages [0, K), source stream) and the back warp
+// ([K, 2T), stores) do unequal work.  A CTA's warp w runs on sub-partition
+// (SMSP) w % 4 of its SM, so with fixed roles every resident CTA would put its
+// fronts on the same two SMSPs and its backs on the other two.  The roles of
+// a CTA are therefore swapped when its hardware warp slot (%warpid of warp 0,
+// 4 slots per CTA) is odd, so each SMSP hosts fronts and backs of different
+// CTAs (SOR_WAVE_MIX=0 at build time: fixed roles).
+#ifndef SOR_WAVE_MIX
+#define SOR_WAVE_MIX 0
+#endif
+
+template <typename R, int T, int NST, int CK, bool SPLIT, int NC, bool LINK>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
     wave_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
   const int bid = (int)blockIdx.x - ctl.defer;
@@ -1098,7 +1135,17 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int slot = SPLIT ? warp >> 1 : warp;  // tile slot within the CTA
-  const int role = SPLIT ? warp & 1 : 0;      // 0 front (or whole), 1 back
+  int role = SPLIT ? warp & 1 : 0;            // 0 front (or whole), 1 back
+  if (SPLIT && SOR_WAVE_MIX) {
+    __shared__ int cta_swap;
+    if (threadIdx.x == 0) {
+      unsigned wid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      cta_swap = (int)((wid >> 2) & 1u);
+    }
+    __syncthreads();
+    role ^= cta_swap;
+  }
   const int gw = bid * wave_tiles_per_cta(SPLIT) + slot;
   // the tile table is written once by the host: read it before waiting on the
   // previous launch, so its latency overlaps that wait and the stop read
@@ -1136,7 +1183,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     // i_first even; nsteps a multiple of 6 (ring phase x parity)
     const int i_first = (R0 - (2 * T - 1)) & ~1;
     const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
-    if (role == 0) tile_halo_wait(a, sw, WC, R0, R1, 2 * T, lane, ctl.st);
+    if (LINK && role == 0) tile_halo_wait(a, sw, WC, R0, R1, 2 * T, lane, ctl.st);
     if (SPLIT) {
       unsigned char* pbase = wave_smem + slot * wave_smem_per_pair<R, NST, NC>();
       R* hand = reinterpret_cast<R*>(pbase + wave_smem_per_warp<R, NST, NC>());
@@ -1151,7 +1198,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
       wave_tile<R, T, NST, CK, 0, 2 * T, NC>(a, tm.m, wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
     }
   }
-  if (a.link.on && (!SPLIT || (threadIdx.x >> 5) & 1)) {
+  if (LINK && (!SPLIT || role == 1)) {
     // re-read the tile (nothing of it stays live across the stream loop)
     const int gw2 = ((int)blockIdx.x - ctl.defer) * wave_tiles_per_cta(SPLIT) + (SPLIT ? (int)(threadIdx.x >> 6) : (int)(threadIdx.x >> 5));
     if ((int)blockIdx.x >= ctl.defer && gw2 < a.ntiles) {
@@ -1318,7 +1365,7 @@ struct JacobiPipe {
   }
 };
 
-template <typename R, int T, int NST, int CK>
+template <typename R, int T, int NST, int CK, bool LINK>
 __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
     jacobi_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1348,7 +1395,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
     const int R0 = tile.y, R1 = tile.z;
     const int i_first = (R0 - (T - 1)) & ~1;
     const int nsteps = (R1 + T - 1 - i_first + 5) / 6 * 6;
-    tile_halo_wait(a, sw, WC, R0, R1, T, lane, ctl.st);
+    if (LINK) tile_halo_wait(a, sw, WC, R0, R1, T, lane, ctl.st);
     unsigned char* wbase = wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
     Pipe P;
 #pragma unroll
@@ -1407,7 +1454,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, T <= 2 ? 4 : 3)
 #pragma unroll
     for (int t = 0; t < Pipe::NSLOT; ++t) dm[t] = P.dmax[t];
   }
-  if (a.link.on) {
+  if (LINK) {
     const int gw2 = ((int)blockIdx.x - ctl.defer) * kWaveWarps + (int)(threadIdx.x >> 5);
     if ((int)blockIdx.x >= ctl.defer && gw2 < a.ntiles) {
       const int4 t2 = a.tiles[gw2];

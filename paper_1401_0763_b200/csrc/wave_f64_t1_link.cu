@@ -1,0 +1,8 @@
+// wave_f64_t1_link.cu — wave_kernel<double, T=1, LINK=true> and its launcher (see wave_launch.cuh).
+#include "wave_launch.cuh"
+
+namespace sorh {
+template int launch_wave_T<double, 1, 0, true>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave_T<double, 1, 1, true>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave_T<double, 1, 2, true>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+}  // namespace sorh

@@ -10,7 +10,7 @@ namespace sorh {
 template <typename R>
 constexpr int wave_nst() { return 14; }
 
-template <typename R, int T, int CK, bool SPLIT, int NC>
+template <typename R, int T, int CK, bool SPLIT, int NC, bool LINK>
 int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   constexpr int NST = wave_nst<R>();
   constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
@@ -18,8 +18,8 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   static int occ_dev[kMaxDev] = {};  // resident CTAs/SM for this instance, per device
   int& occ = occ_dev[g->device % kMaxDev];
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT, NC>, kWaveWarps * 32, smem);
+    CU(cudaFuncSetAttribute(wave_kernel<R, T, NST, CK, SPLIT, NC, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_kernel<R, T, NST, CK, SPLIT, NC, LINK>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -55,21 +55,21 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   cfg.attrs = at;
   // PDL only for one-wave launches (wave_pdl)
   cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC>, a, c, s.tmap[g->cur]));
+  CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC, LINK>, a, c, s.tmap[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
 
-template <typename R, int T, int CK>
+template <typename R, int T, int CK, bool LINK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   // 4 columns per lane: wider lanes (NC = 6, 8; bitwise equal) measured
   // slower on B200 at every T (fewer resident warps outweigh the extra ILP).
   // T >= 2: warp pairs (split).
-  return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC>(g, s, w, ctl, fused_fin);
+  return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC, LINK>(g, s, w, ctl, fused_fin);
 }
 
 // Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
-template <typename R, int T, int CK>
+template <typename R, int T, int CK, bool LINK>
 int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {
   constexpr int NST = wave_nst<R>();
   constexpr int smem = kWaveWarps * wave_smem_per_warp<R, NST, kWaveNC>();
@@ -77,8 +77,8 @@ int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_f
   static int occ_dev[kMaxDev] = {};
   int& occ = occ_dev[g->device % kMaxDev];
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(jacobi_kernel<R, T, NST, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_kernel<R, T, NST, CK>, kWaveWarps * 32, smem);
+    CU(cudaFuncSetAttribute(jacobi_kernel<R, T, NST, CK, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_kernel<R, T, NST, CK, LINK>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -113,7 +113,7 @@ int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_f
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK>, a, c, s.tmap[g->cur]));
+  CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK, LINK>, a, c, s.tmap[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
