@@ -21,9 +21,10 @@ struct sor3d_grid {
   int64_t pitch = 0;
   void* plane = nullptr;        // the current iterate
   void* plane2 = nullptr;       // FUSED kernel: the other plane of the ping-pong
-  // default NATURAL: the fused z-wavefront is bitwise equal but slower on
-  // B200 (f64 57 vs 158 GLUP/s at 512^3: the correctly rounded division on its
-  // per-plane critical path, one CTA barrier per plane)
+  // default NATURAL: the fused z-plane wavefront (one HBM pass per
+  // iteration) is bitwise equal but slower on B200 (f64 86 vs 158 GLUP/s at
+  // 512^3, profiles/r2_sor3d_fused_variants.txt): one CTA barrier per plane
+  // leaves each CTA latency-bound and only two CTAs fit per SM
   int kernel = SOR_KERNEL_NATURAL;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, poll_ev[2] = {nullptr, nullptr};
@@ -91,16 +92,31 @@ int load3d(sor3d_grid* g, const double* init) {
 template <typename R>
 int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
   if (g->kernel == SOR_KERNEL_FUSED) {
-    dim3 grid((unsigned)((g->nx + 2 + kX3 - 1) / kX3), (unsigned)((g->ny + 2 + kY3 - 1) / kY3));
+    using G = K3Geo<kX3, kY3>;
+    const unsigned bx = (unsigned)((g->nx + 2 + kX3 - 1) / kX3), by = (unsigned)((g->ny + 2 + kY3 - 1) / kY3);
+    // z chunks: about two waves of resident CTAs, at least 8 planes each
+    static int occ_dev[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& occ = occ_dev[dev % kMaxDev];
+    if (occ == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3d_fused<R, false, kX3, kY3>, G::NT, 0);
+      if (occ <= 0) occ = 1;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = std::max<int64_t>(1, (2LL * occ * nsm + bx * by - 1) / ((int64_t)bx * by));
+    const int zc = (int)std::max<int64_t>(8, (g->nz + want - 1) / want);
+    dim3 grid(bx, by, (unsigned)((g->nz + zc - 1) / zc));
     IterCtl c = ctl;
     c.finalize = ctl.ck ? 1 : 0;
-    c.nparts = grid.x * grid.y;
+    c.nparts = grid.x * grid.y * grid.z;
     if (ctl.ck)
-      k3d_fused<R, true><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
-                                                             (int)g->nz, (int)g->ny, (int)g->nx, w, c);
+      k3d_fused<R, true, kX3, kY3><<<grid, G::NT, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
+                                                                  (int)g->nz, (int)g->ny, (int)g->nx, zc, w, c);
     else
-      k3d_fused<R, false><<<grid, kW3P * kW3Y, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
-                                                              (int)g->nz, (int)g->ny, (int)g->nx, w, c);
+      k3d_fused<R, false, kX3, kY3><<<grid, G::NT, 0, g->stream>>>((const R*)g->plane, (R*)g->plane2, g->pitch,
+                                                                   (int)g->nz, (int)g->ny, (int)g->nx, zc, w, c);
     CU3(cudaGetLastError());
     std::swap(g->plane, g->plane2);
     return SOR_OK;

@@ -402,6 +402,7 @@ void free_grid(sor_grid* g) {
   if (g->hstate) cudaFreeHost(g->hstate);
   if (g->scratch) cudaFree(g->scratch);
   if (g->dflag) cudaFree(g->dflag);
+  if (g->gbar) cudaFree(g->gbar);
   if (g->flagbuf) cudaFree(g->flagbuf);
   if (g->djoin) cudaFree(g->djoin);
   if (g->ev0) cudaEventDestroy(g->ev0);
@@ -439,6 +440,7 @@ int build(sor_grid* g, const std::vector<std::pair<int64_t, int64_t>>& spans, in
   CU(cudaMallocHost(&g->hstate, 2 * sizeof(DevState)));
   memset(g->hstate, 0, 2 * sizeof(DevState));
   CU(cudaMalloc(&g->dflag, sizeof(unsigned int)));
+  CU(cudaMalloc(&g->gbar, sizeof(unsigned int)));
   g->scratch_bytes = (size_t)std::max<int64_t>(64 << 20, (g->cols + 2) * 8 * 4);
   if (g->dt == SOR_F32 || g->mode == Mode::Dist) {
     cudaError_t e = cudaMalloc(&g->scratch, g->scratch_bytes);
@@ -1254,6 +1256,39 @@ int solve_ck(int T) {
   return ck == 3 ? 3 : 4;
 }
 
+// K6 eligibility: one slab, SOR, both planes L2-resident (the persistent
+// kernel's passes re-read what the previous pass wrote; beyond L2 a pass is
+// HBM-bound and the per-launch overhead is already amortised).
+// SOR_NO_PERSIST=1 disables it.
+bool use_persist(const sor_grid* g) {
+  static int off = -1;
+  if (off < 0) off = getenv("SOR_NO_PERSIST") ? 1 : 0;
+  if (off || g->persist_off || !single_part(g) || g->method != 0 || !g->gbar) return false;
+  const Slab& s = g->slabs[0];
+  const double planes = 2.0 * (double)s.nstore * (double)g->pitch * (double)g->esz;
+  return planes <= 48.0 * (1 << 20);
+}
+
+template <typename R>
+int persist_passes(sor_grid* g, R w, int T, int npasses) {
+  const Slab& s = g->slabs[0];
+  int rc = SOR_E_INVAL;
+  switch (T) {
+    case 1: rc = launch_wave_persist<R, 1>(g, s, w, npasses, g->gbar); break;
+    case 2: rc = launch_wave_persist<R, 2>(g, s, w, npasses, g->gbar); break;
+    case 3: rc = launch_wave_persist<R, 3>(g, s, w, npasses, g->gbar); break;
+    case 4: rc = launch_wave_persist<R, 4>(g, s, w, npasses, g->gbar); break;
+  }
+  if (rc != SOR_OK) return rc;
+  // the kernel alternates between the current plane and the next one (also
+  // when a third plane exists for the deferred stop test)
+  if (npasses & 1) g->cur = g->nxt(g->cur);
+  g->st.half_sweeps += (int64_t)2 * T * npasses;
+  g->st.hbm_passes += npasses;
+  g->seq += npasses;
+  return SOR_OK;
+}
+
 // Enqueue iterations [k_from, k_to] (1-based within the call).
 //  - iterate (base.solve == 0): passes of up to T; the last one reports its
 //    last iteration's max-change if check_last.
@@ -1288,6 +1323,20 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
       const int64_t left = end - k + 1;
       int t = (int)(left % T);  // remainder first, so a block ends on a full pass
       if (t == 0) t = T;
+      if (t == T && !base.solve) {
+        // K6: the full passes of an iterate block as one persistent launch
+        // (all but a measured last pass)
+        const int64_t full = left / T - ((check_last && end == k_to) ? 1 : 0);
+        if (full >= 2 && use_persist(g)) {
+          const int rc = persist_passes<R>(g, w, T, (int)std::min<int64_t>(full, 1 << 20));
+          if (rc == SOR_OK) {
+            k += std::min<int64_t>(full, 1 << 20) * T;
+            continue;
+          }
+          if (rc != SOR_E_UNSUPPORTED) return rc;
+          g->persist_off = true;  // tiles do not fit in one wave: pass by pass from now on
+        }
+      }
       IterCtl c = base;
       c.k_last = k + t - 1;
       c.T = t;

@@ -85,6 +85,8 @@ struct sor_grid {
   double* scratch = nullptr;         // f64 staging for f32 pack/unpack and dist scatter/gather
   size_t scratch_bytes = 0;
   unsigned int* dflag = nullptr;
+  unsigned int* gbar = nullptr;  // K6: grid-barrier counter of the persistent kernel
+  bool persist_off = false;      // K6 tiles did not fit in one wave on this handle
   int rank = 0, nranks = 1;
   sorh::Transport transport = sorh::Transport::None;
   ncclComm_t comm = nullptr;
@@ -179,5 +181,7 @@ template <typename R, int T, int CK, bool LINK>
 int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin);
 template <typename R, int T, int CK, bool LINK>
 int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin);
+template <typename R, int T>
+int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar);
 
 }  // namespace sorh

@@ -134,6 +134,37 @@ __device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b)
 __device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b); }
 
+// s/6 correctly rounded (reading N3-1) without the division routine: the
+// quotient q0 = RN(s*RN(1/6)) is corrected once with its exact remainder
+// r = s - 6*q0 (an FMA), q = RN(q0 + r*RN(1/6)) (Markstein).  Verified equal
+// to the IEEE division for every float32 with a normal quotient (exhaustive)
+// and 5e8 random float64 (tools/div6_check.c).  Zeros keep their sign
+// (select); subnormal quotients, inf and NaN take the division (a branch that
+// realistic grids never take).  The FMAs here are the algorithm, not a
+// contraction of the canonical update.
+__device__ __forceinline__ double div6(double s) {
+  const double yi = 1.0 / 6.0;
+  const double q0 = __dmul_rn(s, yi);
+  const double r = __fma_rn(-q0, 6.0, s);
+  const double q1 = __fma_rn(r, yi, q0);
+  const double a = fabs(s);
+  const bool fast = a >= 0x1.8p-1020 && a <= 0x1.fffffffffffffp+1023;
+  double q = fast ? q1 : s;  // s == +-0: q = s exactly
+  if (!fast && s != 0.0) q = __ddiv_rn(s, 6.0);
+  return q;
+}
+__device__ __forceinline__ float div6(float s) {
+  const float yi = 1.0f / 6.0f;
+  const float q0 = __fmul_rn(s, yi);
+  const float r = __fmaf_rn(-q0, 6.0f, s);
+  const float q1 = __fmaf_rn(r, yi, q0);
+  const float a = fabsf(s);
+  const bool fast = a >= 0x1.8p-124f && a <= 0x1.fffffep+127f;
+  float q = fast ? q1 : s;
+  if (!fast && s != 0.0f) q = __fdiv_rn(s, 6.0f);
+  return q;
+}
+
 // Eq. 1, BJ form, canonical order.  ns = uN+uS and we = uW+uE are formed by the
 // caller (addition is commutative, so which operand is W and which E is moot).
 template <typename R>
@@ -1232,6 +1263,88 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
   }
 }
 
+// ---------------------------------------------------------------- persistent (K6)
+// L2-resident grids (C2: two 8 MB planes): the launch, ramp and drain of one
+// wave launch per pass cost more than the pass itself.  One cooperative
+// launch runs `npasses` T-deep passes; the CTAs meet at a grid barrier
+// between passes (the paper's per-phase barrier [P:314, P:317] once per T
+// iterations), alternating the planes.  Each pass is the wave kernel's tile
+// pass (same tiles, same stages), so the result is bitwise the same.
+__device__ __forceinline__ void mbar_inval(uint32_t bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// All CTAs of a cooperative launch: arrive, then wait until `target` CTAs
+// arrived in total (the counter only grows during a launch).
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    while (ld_acquire_gpu_u32(ctr) < target) {
+    }
+  }
+  __syncthreads();
+  // the next pass reads rows other CTAs just wrote (generic proxy) with TMA
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <typename R, int T, int NST, bool SPLIT, int NC>
+__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
+    wave_persist_kernel(WaveArgs<R> a, int npasses, unsigned* gbar, const __grid_constant__ WaveMaps tmA,
+                        const __grid_constant__ WaveMaps tmB) {
+  extern __shared__ __align__(128) unsigned char wave_smem[];
+  constexpr int WC = wave_cols<NC>();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int slot = SPLIT ? warp >> 1 : warp;
+  const int role = SPLIT ? warp & 1 : 0;
+  const int gw = (int)blockIdx.x * wave_tiles_per_cta(SPLIT) + slot;
+  const bool has_tile = gw < a.ntiles;
+  const int4 tile = has_tile ? a.tiles[gw] : make_int4(0, 0, 0, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  unsigned long long dm[kMaxT] = {};
+  for (int p = 0; p < npasses; ++p) {
+    WaveArgs<R> ap = a;
+    if (p & 1) {
+      ap.src = a.dst;
+      ap.dst = const_cast<R*>(a.src);
+    }
+    const CUtensorMap* tm = (p & 1) ? tmB.m : tmA.m;
+    if (has_tile) {
+      const int sw = a.s0 + tile.x * (WC - 4 * T);
+      const int R0 = tile.y, R1 = tile.z;
+      const int i_first = (R0 - (2 * T - 1)) & ~1;
+      const int nsteps = (R1 + 2 * T - 1 - i_first + 5) / 6 * 6;
+      unsigned char* base = SPLIT ? wave_smem + slot * wave_smem_per_pair<R, NST, NC>()
+                                  : wave_smem + warp * wave_smem_per_warp<R, NST, NC>();
+      if (SPLIT) {
+        R* hand = reinterpret_cast<R*>(base + wave_smem_per_warp<R, NST, NC>());
+        const int bar_id = 1 + 4 * slot;
+        constexpr int K = wave_split_stage(T);
+        if (role == 0)
+          wave_tile<R, T, NST, 0, 0, K, NC>(ap, tm, base, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+        else
+          wave_tile<R, T, NST, 0, K, 2 * T, NC>(ap, tm, base, hand, bar_id, lane, sw, R0, R1, i_first, nsteps, dm);
+      } else {
+        wave_tile<R, T, NST, 0, 0, 2 * T, NC>(ap, tm, base, nullptr, 0, lane, sw, R0, R1, i_first, nsteps, dm);
+      }
+      // the tile's mbarriers are initialised again by the next pass's tile
+      if (role == 0 && lane == 0) {
+        const uint32_t bar = smem_u32(base) + NST * WC * (uint32_t)sizeof(R);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) mbar_inval(bar + 8u * k);
+      }
+    }
+    if (p + 1 < npasses) grid_barrier(gbar, (unsigned)(p + 1) * gridDim.x);
+  }
+}
+
 // ---------------------------------------------------------------- Jacobi (NEXT-2)
 // Jacobi [P:95, S:179-187] on the same layout, tiles and TMA source ring as
 // the wave kernel: X_k from X_{k-1} only, X = 0.25*((N+S)+(W+E)).  T
@@ -1504,7 +1617,7 @@ __global__ void __launch_bounds__(256) k3d_half_sweep(R* base, long long pitch, 
     R* uc = base + (long long)z * plane + (long long)y * pitch + x;
     const R u = uc[0];
     const R s = radd(radd(radd(uc[-pitch], uc[pitch]), radd(uc[-1], uc[1])), radd(uc[-plane], uc[plane]));
-    const R a = rdiv(s, R(6));
+    const R a = div6(s);
     const R un = radd(u, rmul(w, rsub(a, u)));
     if (CHECK) dmax = delta_bits(un, u);
     uc[0] = un;
@@ -1523,94 +1636,123 @@ __global__ void __launch_bounds__(256) k3d_half_sweep(R* base, long long pitch, 
   }
 }
 
-// Fused 3-D iteration (K3 form): one HBM pass per iteration, src -> dst.  A
-// CTA owns an kX3 x kY3 tile of (y, x) columns and marches down z; each
-// thread holds a PAIR of x-adjacent columns of a (kY3+4) x (kX3+4) window, so
-// in every plane one of its two cells is red and the other black (no
-// divergence between the colour phases).  Step z: the red half-sweep at plane
-// z (the tile plus a 1-column ring, whose new reds the tile's blacks need)
-// from the source, then the black half-sweep at plane z-1 (tile only) from the
-// new reds of planes z-2, z-1, z; plane z-1 of the tile is then final and
-// stored.  In-plane neighbours come from double-buffered shared planes
-// (source plane z, plane z after its red phase); vertical ones from the
-// thread's registers; source planes are loaded kPF steps ahead.  One
-// __syncthreads per step.  Bitwise equal to the two-phase sweep: every cell
-// reads exactly the values the in-place red-then-black order gives it.
-constexpr int kX3 = 64, kY3 = 8;
-constexpr int kW3X = kX3 + 4, kW3Y = kY3 + 4;  // window (columns)
-constexpr int kW3P = kW3X / 2;                 // column pairs per window row
+// Fused 3-D iteration (K3 form, one HBM pass per iteration, src -> dst).  A
+// CTA owns a KX x KY tile of (y, x) columns and a chunk [z0, z1) of planes and
+// marches up z; each thread holds a PAIR of x-adjacent columns of the
+// (KY+4) x (KX+4) window (the tile and a 2-cell ring), so in every plane one
+// of its two cells is red and the other black (no divergence between the
+// colour phases).  Step z: the red half-sweep at plane z (tile + 1-cell ring,
+// whose new reds the tile's blacks need) from the source planes z-1, z, z+1,
+// then the black half-sweep at plane z-1 (tile only) from the new reds of
+// planes z-2, z-1, z; plane z-1 of the tile is then final and stored.
+// In-plane neighbours come from shared planes (source plane z and the reds of
+// plane z-1, double-buffered by z parity), vertical ones from the thread's
+// registers; one __syncthreads per plane.  The chunk's first step computes
+// the reds of plane z0-1 (the neighbouring chunk owns them; both compute the
+// same values from the source), so chunks never synchronise.  Bitwise equal
+// to the two-phase sweep: every cell reads exactly the values the in-place
+// red-then-black order gives it.
+template <int KX, int KY>
+struct K3Geo {
+  static constexpr int WX = KX + 4, WY = KY + 4;  // window (columns, rows)
+  static constexpr int WP = WX / 2;               // column pairs per window row
+  static constexpr int NT = WP * WY;              // threads per CTA
+};
+#ifndef SOR_K3_X
+#define SOR_K3_X 32
+#endif
+#ifndef SOR_K3_Y
+#define SOR_K3_Y 16
+#endif
+#ifndef SOR_K3_PF
+#define SOR_K3_PF 2
+#endif
+constexpr int kX3 = SOR_K3_X, kY3 = SOR_K3_Y;  // tile of the fused 3-D kernel
 
-template <typename R, bool CHECK>
-__global__ void __launch_bounds__(kW3P * kW3Y, 3)
-    k3d_fused(const R* __restrict__ src, R* __restrict__ dst, long long pitch, int nz, int ny, int nx, R w,
+template <typename R, bool CHECK, int KX, int KY>
+__global__ void __launch_bounds__(K3Geo<KX, KY>::NT)
+    k3d_fused(const R* __restrict__ src, R* __restrict__ dst, long long pitch, int nz, int ny, int nx, int zc, R w,
               IterCtl ctl) {
+  using G = K3Geo<KX, KY>;
   if (ctl.st && ctl.solve && ld_stop(ctl.st)) return;
-  __shared__ R s_src[2][kW3Y][kW3X];  // source plane z (by z parity)
-  __shared__ R s_red[2][kW3Y][kW3X];  // plane z after its red phase (by z parity)
-  const int tp = threadIdx.x % kW3P, ty = threadIdx.x / kW3P;
+  __shared__ R s_src[2][G::WY][G::WX];  // source plane z (by z parity)
+  __shared__ R s_red[2][G::WY][G::WX];  // plane z after its red phase (by z parity)
+  const int tp = threadIdx.x % G::WP, ty = threadIdx.x / G::WP;
   const int tx0 = 2 * tp;  // window column of the pair's first cell
-  const int x0 = blockIdx.x * kX3 - 2 + tx0, y = blockIdx.y * kY3 - 2 + ty;
+  const int x0 = blockIdx.x * KX - 2 + tx0, y = blockIdx.y * KY - 2 + ty;
+  const int z0 = 1 + blockIdx.z * zc, z1 = min(nz + 1, z0 + zc);  // owned planes [z0, z1)
   bool inside[2], interior[2], ring1[2], tile[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int x = x0 + e, tx = tx0 + e;
     inside[e] = x >= 0 && x <= nx + 1 && y >= 0 && y <= ny + 1;
     interior[e] = x >= 1 && x <= nx && y >= 1 && y <= ny;
-    ring1[e] = tx >= 1 && tx <= kX3 + 2 && ty >= 1 && ty <= kY3 + 2;
-    tile[e] = tx >= 2 && tx < kX3 + 2 && ty >= 2 && ty < kY3 + 2;
+    ring1[e] = tx >= 1 && tx <= KX + 2 && ty >= 1 && ty <= KY + 2;
+    tile[e] = tx >= 2 && tx < KX + 2 && ty >= 2 && ty < KY + 2;
   }
+  const bool both = inside[0] && inside[1];
   const long long plane = (long long)(ny + 2) * pitch;
   const long long col = (long long)y * pitch + x0;
-  auto ld = [&](int z, int e) -> R {
-    return (inside[e] && z <= nz + 1) ? src[(long long)z * plane + col + e] : R(0);
+  // the pair of plane z (zero outside the grid); one 16-B load when both
+  // cells are inside (x0 even: aligned)
+  auto ld = [&](int z, R (&v)[2]) {
+    v[0] = v[1] = R(0);
+    if (z < 0 || z > nz + 1) return;
+    const R* p = src + (long long)z * plane + col;
+    if (both) {
+      if (sizeof(R) == 8) {
+        const double2 d = *reinterpret_cast<const double2*>(p);
+        v[0] = (R)d.x;
+        v[1] = (R)d.y;
+      } else {
+        const float2 d = *reinterpret_cast<const float2*>(p);
+        v[0] = (R)d.x;
+        v[1] = (R)d.y;
+      }
+    } else {
+      if (inside[0]) v[0] = p[0];
+      if (inside[1]) v[1] = p[1];
+    }
   };
-  constexpr int kPF = 4;
+  constexpr int kPF = SOR_K3_PF;  // source planes in flight ahead of the step
   R q[kPF][2];
   R sm1[2], s0[2], n2[2], n1[2];
+  ld(z0 - 2, sm1);
+  ld(z0 - 1, s0);
+  n2[0] = n2[1] = n1[0] = n1[1] = R(0);
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    sm1[e] = ld(0, e);
-    s0[e] = ld(1, e);
-    n2[e] = n1[e] = sm1[e];  // plane 0 is the shell: fixed
-#pragma unroll
-    for (int k = 0; k < kPF; ++k) q[k][e] = ld(2 + k, e);
-  }
+  for (int k = 0; k < kPF; ++k) ld(z0 + k, q[k]);
   unsigned long long dmax = 0ull;
   auto step = [&](int z, R (&qs)[2]) {
-    R sp1[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      sp1[e] = qs[e];           // plane z+1
-      qs[e] = ld(z + 1 + kPF, e);
-    }
+    R sp1[2] = {qs[0], qs[1]};  // plane z+1
+    ld(z + 1 + kPF, qs);
     const int pz = z & 1;
     s_src[pz][ty][tx0] = s0[0];
     s_src[pz][ty][tx0 + 1] = s0[1];
     __syncthreads();
     // red phase at plane z: the pair's cell e with (z + y + x0 + e) even
-    // (selects, not indexing: a runtime index would put the pair in local memory)
     const bool e1 = ((z + y + x0) & 1) != 0;  // the red cell is the pair's second
     R nz0[2] = {s0[0], s0[1]};
     {
       const int tx = tx0 + (e1 ? 1 : 0);
       const bool upd = e1 ? (ring1[1] && interior[1]) : (ring1[0] && interior[0]);
-      if (z <= nz && upd) {
+      if (z >= 1 && z <= nz && upd) {
         const R sv = e1 ? s0[1] : s0[0];
         const R s = radd(radd(radd(s_src[pz][ty - 1][tx], s_src[pz][ty + 1][tx]),
                               radd(s_src[pz][ty][tx - 1], s_src[pz][ty][tx + 1])),
                          radd(e1 ? sm1[1] : sm1[0], e1 ? sp1[1] : sp1[0]));
-        const R v = radd(sv, rmul(w, rsub(rdiv(s, R(6)), sv)));
+        const R v = radd(sv, rmul(w, rsub(div6(s), sv)));
         nz0[0] = e1 ? nz0[0] : v;
         nz0[1] = e1 ? v : nz0[1];
-        if (CHECK && (e1 ? tile[1] : tile[0])) dmax = umax64(dmax, delta_bits(v, sv));
+        if (CHECK && z >= z0 && z < z1 && (e1 ? tile[1] : tile[0])) dmax = umax64(dmax, delta_bits(v, sv));
       }
     }
     s_red[pz][ty][tx0] = nz0[0];
     s_red[pz][ty][tx0 + 1] = nz0[1];
     // black phase at plane z-1: the pair's cell with (z-1 + y + x) odd, i.e.
     // the red index of plane z; its neighbours are reds: in-plane ones of
-    // plane z-1 (shared, previous step), vertical ones of planes z-2, z
-    if (z - 1 >= 1) {
+    // plane z-1 (shared, written last step), vertical ones of planes z-2, z
+    if (z - 1 >= z0) {
       const int tx = tx0 + (e1 ? 1 : 0);
       R out[2] = {n1[0], n1[1]};
       if (e1 ? (tile[1] && interior[1]) : (tile[0] && interior[0])) {
@@ -1619,15 +1761,22 @@ __global__ void __launch_bounds__(kW3P * kW3Y, 3)
         const R s = radd(radd(radd(s_red[qz][ty - 1][tx], s_red[qz][ty + 1][tx]),
                               radd(s_red[qz][ty][tx - 1], s_red[qz][ty][tx + 1])),
                          radd(e1 ? n2[1] : n2[0], e1 ? nz0[1] : nz0[0]));
-        const R v = radd(ub, rmul(w, rsub(rdiv(s, R(6)), ub)));
+        const R v = radd(ub, rmul(w, rsub(div6(s), ub)));
         out[0] = e1 ? out[0] : v;
         out[1] = e1 ? v : out[1];
         if (CHECK) dmax = umax64(dmax, delta_bits(v, ub));
       }
       R* o = dst + (long long)(z - 1) * plane + col;
+      if (tile[0] && tile[1] && both) {
+        if (sizeof(R) == 8)
+          *reinterpret_cast<double2*>(o) = make_double2((double)out[0], (double)out[1]);
+        else
+          *reinterpret_cast<float2*>(o) = make_float2((float)out[0], (float)out[1]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (tile[e] && inside[e]) o[e] = out[e];
+        for (int e = 0; e < 2; ++e)
+          if (tile[e] && inside[e]) o[e] = out[e];
+      }
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -1637,14 +1786,14 @@ __global__ void __launch_bounds__(kW3P * kW3Y, 3)
       s0[e] = sp1[e];
     }
   };
-  for (int z = 1; z <= nz + 1; z += kPF) {
+  for (int z = z0 - 1; z <= z1; z += kPF) {
 #pragma unroll
     for (int k = 0; k < kPF; ++k)
-      if (z + k <= nz + 1) step(z + k, q[k]);
+      if (z + k <= z1) step(z + k, q[k]);
   }
   if (CHECK) {
     dmax = warp_max_u64(dmax);
-    __shared__ unsigned long long wmax[(kW3P * kW3Y + 31) / 32];
+    __shared__ unsigned long long wmax[(G::NT + 31) / 32];
     if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -5,4 +5,5 @@ namespace sorh {
 template int launch_wave_T<float, 1, 0, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 1, 1, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 1, 2, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
+template int launch_wave_persist<float, 1>(sor_grid*, const Slab&, float, int, unsigned*);
 }  // namespace sorh

@@ -7,4 +7,5 @@ template int launch_wave_T<float, 2, 1, false>(sor_grid*, const Slab&, float, co
 template int launch_wave_T<float, 2, 2, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 2, 3, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 2, 4, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
+template int launch_wave_persist<float, 2>(sor_grid*, const Slab&, float, int, unsigned*);
 }  // namespace sorh

@@ -7,4 +7,5 @@ template int launch_wave_T<float, 3, 1, false>(sor_grid*, const Slab&, float, co
 template int launch_wave_T<float, 3, 2, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 3, 3, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
 template int launch_wave_T<float, 3, 4, false>(sor_grid*, const Slab&, float, const IterCtl&, bool);
+template int launch_wave_persist<float, 3>(sor_grid*, const Slab&, float, int, unsigned*);
 }  // namespace sorh

@@ -7,4 +7,5 @@ template int launch_wave_T<double, 2, 1, false>(sor_grid*, const Slab&, double, 
 template int launch_wave_T<double, 2, 2, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
 template int launch_wave_T<double, 2, 3, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
 template int launch_wave_T<double, 2, 4, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave_persist<double, 2>(sor_grid*, const Slab&, double, int, unsigned*);
 }  // namespace sorh

@@ -7,4 +7,5 @@ template int launch_wave_T<double, 3, 1, false>(sor_grid*, const Slab&, double, 
 template int launch_wave_T<double, 3, 2, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
 template int launch_wave_T<double, 3, 3, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
 template int launch_wave_T<double, 3, 4, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave_persist<double, 3>(sor_grid*, const Slab&, double, int, unsigned*);
 }  // namespace sorh

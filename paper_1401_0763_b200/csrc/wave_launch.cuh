@@ -68,6 +68,71 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
   return launch_wave_TS<R, T, CK, (T >= 2), kWaveNC, LINK>(g, s, w, ctl, fused_fin);
 }
 
+// K6: `npasses` T-deep passes in one cooperative launch (L2-resident grids;
+// see wave_persist_kernel).  Returns SOR_E_UNSUPPORTED if the tiles do not fit
+// in one wave of co-resident CTAs (the caller then launches pass by pass).
+template <typename R, int T>
+int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar) {
+  constexpr int NST = wave_nst<R>();
+  constexpr bool SPLIT = T >= 2;
+  constexpr int NC = kWaveNC;
+  constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
+  constexpr int per_cta = wave_tiles_per_cta(SPLIT);
+  static int occ_dev[kMaxDev] = {};
+  int& occ = occ_dev[g->device % kMaxDev];
+  if (occ == 0) {
+    CU(cudaFuncSetAttribute(wave_persist_kernel<R, T, NST, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_persist_kernel<R, T, NST, SPLIT, NC>, kWaveWarps * 32,
+                                                  smem);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[0]);
+  a.dst = col0<R>(s.plane[1]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = w;
+  a.s0 = -4 * ((2 * T + 3) / 4);
+  // tiles per SM: half the one-wave budget of an ordinary launch (taller
+  // bands, less warm-up per pass; measured best on C2 at T = 3, 4:
+  // profiles/r2_c2_persistent.txt); SOR_PERSIST_TPS overrides
+  static int tps = -1;
+  if (tps < 0) {
+    const char* e = getenv("SOR_PERSIST_TPS");
+    tps = e ? atoi(e) : 0;
+  }
+  const int budget = tps > 0 ? std::min(tps, occ * per_cta) : std::max(1, occ * per_cta / 2);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, 0, 2 * T, 2 * T, wave_cols<NC>(), budget, SPLIT, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta);
+  if (blocks > (unsigned)(occ * g->nsm)) return SOR_E_UNSUPPORTED;
+  // planes alternate pass by pass starting from the current one
+  const int p0 = g->cur, p1 = g->nxt(g->cur);
+  a.src = col0<R>(s.plane[p0]);
+  a.dst = col0<R>(s.plane[p1]);
+  CU(cudaMemsetAsync(gbar, 0, sizeof(unsigned), g->stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, wave_persist_kernel<R, T, NST, SPLIT, NC>, a, npasses, gbar, s.tmap[p0], s.tmap[p1]));
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
 // Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
 template <typename R, int T, int CK, bool LINK>
 int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin) {

@@ -161,21 +161,28 @@ def test_paper_replay(gpu, orc):
     assert r.max_change < 1e-5 and abs(r.max_change * 28000 / c - 1.0) < 2e-3
 
 
-def test_paper_replay_full_size_bitwise(gpu, orc):
+def test_paper_replay_full_size_bitwise(gpu):
     """NEXT-1 at the paper's own size [P:375, P:383]: 4096 x 4096, north = 1,
     omega = 0.376, eps = 1e-5, K = 4000 -- the whole grid after the converging
-    iteration, the iteration count and the checked max-change, bitwise against
-    the threaded oracle (== serial oracle, pin P14)."""
+    iteration (SHA-256 of the float64 bytes), the iteration count and the
+    checked max-change, bitwise against the threaded oracle (== serial oracle,
+    pin P14).  The oracle's result is stored in tests/golden/ by
+    tools/make_golden_paper_replay.py (oracle only; it needs minutes because
+    fp64 subnormals appear ahead of the under-relaxed front)."""
+    import hashlib
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "paper_replay_4096.json")) as f:
+        gold = json.load(f)
     cfg = SI.config("PAPER")
-    ref = cfg.init()
-    rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, cfg.check_every, threads=THREADS)
     with gpu.Grid.create(cfg.init()) as g:
         g.set_kernel("temporal", 4)
         r = g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every)
         out = g.download()
-    assert (r.converged, r.iters, r.max_change) == (rr.status == 0, rr.iters, rr.max_change)
-    assert rr.iters == 28000
-    assert np.array_equal(out, ref)
+        st = g.stats
+    assert gold["converged"] and gold["iters"] == 28000
+    assert (r.converged, r.iters, r.max_change.hex(), st["checks"]) == (True, gold["iters"], gold["max_change_hex"],
+                                                                         gold["checks"])
+    assert list(out.shape) == gold["shape"] and hashlib.sha256(out.tobytes()).hexdigest() == gold["grid_sha256"]
 
 
 _MULTIWAVE = r"""

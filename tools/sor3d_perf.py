@@ -1,4 +1,5 @@
 """3-D SOR (NEXT-3) throughput (development aid): 512^3 f64/f32, fixed iterations, both kernels."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -16,5 +17,5 @@ for kernel in ("fused", "natural"):
         glups = n ** 3 * iters / best / 1e6
         esz = 8 if dtype == "f64" else 4
         bpu = (2 if kernel == "fused" else 4) * esz
-        print(f"3-D {n}^3 {kernel:8s} {dtype}: {iters} its {best:8.2f} ms {glups:7.1f} GLUP/s "
+        print(f"{os.path.basename(os.environ.get('SOR_LIBRARY', 'default')):14s} 3-D {n}^3 {kernel:8s} {dtype}: {iters} its {best:8.2f} ms {glups:7.1f} GLUP/s "
               f"({glups * bpu:.0f} GB/s algorithmic at {bpu} B/update)", flush=True)
