@@ -38,6 +38,7 @@
 #include <random>
 
 #include "sor_internal.h"
+#include "wave2.cuh"
 
 static_assert(SOR_MAX_T == sorb::kMaxT, "include/sor.h and the kernels disagree on the deepest T");
 
@@ -256,9 +257,12 @@ int make_tmaps(sor_grid* g, Slab& s, int p) {
   const cuuint64_t dims[2] = {(cuuint64_t)g->pitch, (cuuint64_t)s.nstore};
   const cuuint64_t strides[1] = {(cuuint64_t)(g->pitch * g->esz)};
   const cuuint32_t estr[2] = {1u, 1u};
-  for (int b = 0; b < 2; ++b) {
-    const cuuint32_t box[2] = {(cuuint32_t)wave_cols<kWaveNC>(), b == 0 ? 6u : 2u};
-    CUresult r = encode(&s.tmap[p].m[b], g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  for (int b = 0; b < 4; ++b) {
+    // wave kernel: 6-row and 2-row boxes; skew-2 wave kernel: 4-row and 3-row
+    static const cuuint32_t hgt[4] = {6u, 2u, (cuuint32_t)kW2Batch, 3u};
+    const cuuint32_t box[2] = {(cuuint32_t)wave_cols<kWaveNC>(), hgt[b]};
+    CUtensorMap* m = b < 2 ? &s.tmap[p].m[b] : &s.tmap2[p].m[b - 2];
+    CUresult r = encode(m, g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         2, s.plane[p], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(g, SOR_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -1096,8 +1100,20 @@ bool wave_pdl(const sor_grid* g, unsigned blocks, int occ) {
   return !off && (single_part(g) || g->push) && !g->lockstep && blocks <= (unsigned)(occ * g->nsm);
 }
 
+// Skew-2 schedule of the wave kernel (wave2.cuh) for T >= 2: SOR_WAVE2=1
+// selects it (development: bitwise equal, A/B against the skew-1 schedule).
+bool use_wave2(const sor_grid* g, int T) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SOR_WAVE2");
+    on = e ? atoi(e) : 0;
+  }
+  return on != 0 && T >= 2 && !g->push;
+}
+
 template <typename R, int T, int CK>
 int launch_wave_L(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  if (T >= 2 && use_wave2(g, T)) return launch_wave2_T<R, T, CK, false>(g, s, w, ctl, fused_fin);
   return g->push ? launch_wave_T<R, T, CK, true>(g, s, w, ctl, fused_fin)
                  : launch_wave_T<R, T, CK, false>(g, s, w, ctl, fused_fin);
 }

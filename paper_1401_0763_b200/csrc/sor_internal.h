@@ -41,7 +41,8 @@ struct Slab {
   // planes 0, 1: ping-pong; plane 2 (allocated on the first deferred solve,
   // up front for dist-IPC): the speculative pass of the deferred stop test
   void* plane[3] = {nullptr, nullptr, nullptr};
-  WaveMaps tmap[3];  // per plane: tensor maps of the wave kernel's source-row boxes
+  WaveMaps tmap[3];   // per plane: tensor maps of the wave kernel's source-row boxes (6, 2 rows)
+  WaveMaps tmap2[3];  // per plane: the skew-2 wave kernel's boxes (4, 3 rows)
   // device-initiated halo exchange (HaloLink): this slab's flags (released by
   // the neighbours) and the neighbours it pushes to
   unsigned long long* ftop = nullptr;
@@ -183,5 +184,8 @@ template <typename R, int T, int CK, bool LINK>
 int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_fin);
 template <typename R, int T>
 int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar);
+template <typename R, int T, int CK, bool LINK>
+int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin);
+bool use_wave2(const sor_grid* g, int T);
 
 }  // namespace sorh

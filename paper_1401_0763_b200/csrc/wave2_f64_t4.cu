@@ -1,0 +1,10 @@
+// wave2_f64_t4.cu — skew-2 wave2_kernel<double, T=4> and its launcher (see wave2.cuh).
+#include "wave_launch.cuh"
+
+namespace sorh {
+template int launch_wave2_T<double, 4, 0, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave2_T<double, 4, 1, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave2_T<double, 4, 2, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave2_T<double, 4, 3, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+template int launch_wave2_T<double, 4, 4, false>(sor_grid*, const Slab&, double, const IterCtl&, bool);
+}  // namespace sorh

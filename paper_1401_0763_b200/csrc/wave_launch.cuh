@@ -4,6 +4,7 @@
 #pragma once
 
 #include "sor_internal.h"
+#include "wave2.cuh"
 
 namespace sorh {
 
@@ -56,6 +57,58 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   // PDL only for one-wave launches (wave_pdl)
   cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
   CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC, LINK>, a, c, s.tmap[g->cur]));
+  g->st.kernel_launches += 1;
+  return SOR_OK;
+}
+
+// The skew-2 schedule (wave2.cuh): the same tiles and launch protocol.
+template <typename R, int T, int CK, bool LINK>
+int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  constexpr bool SPLIT = T >= 2;
+  constexpr int NC = kWaveNC;
+  constexpr int smem = wave2_smem_bytes<R, SPLIT, NC>();
+  constexpr int per_cta = wave_tiles_per_cta(SPLIT);
+  static int occ_dev[kMaxDev] = {};
+  int& occ = occ_dev[g->device % kMaxDev];
+  if (occ == 0) {
+    CU(cudaFuncSetAttribute(wave2_kernel<R, T, CK, SPLIT, NC, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave2_kernel<R, T, CK, SPLIT, NC, LINK>, kWaveWarps * 32, smem);
+    if (occ <= 0) occ = 1;
+  }
+  WaveArgs<R> a;
+  a.src = col0<R>(s.plane[g->cur]);
+  a.dst = col0<R>(s.plane[g->nxt(g->cur)]);
+  a.pitch = g->pitch;
+  a.g0 = s.g0;
+  a.rows = g->rows;
+  a.cols = g->cols;
+  a.r_lo = s.g_lo;
+  a.r_hi = s.g_hi;
+  a.w = w;
+  a.s0 = -4 * ((2 * T + 3) / 4);
+  const int slab_idx = (int)(&s - &g->slabs[0]);
+  std::pair<int4*, int> tt{nullptr, 0};
+  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
+  a.tiles = tt.first;
+  a.ntiles = tt.second;
+  a.link = make_link(g, s, g->cur, g->nxt(g->cur));
+  record_layout(g, g->nxt(g->cur), a.s0, wave_cols<NC>(), 2 * T, strips_of(g, a.s0, wave_cols<NC>(), 2 * T));
+  const unsigned blocks = (unsigned)((a.ntiles + per_cta - 1) / per_cta) + (ctl.defer ? 1 : 0);
+  IterCtl c = ctl;
+  c.finalize = fused_fin ? 1 : 0;
+  c.nparts = blocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWaveWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, wave2_kernel<R, T, CK, SPLIT, NC, LINK>, a, c, s.tmap2[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
