@@ -57,6 +57,17 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+# SOR_BENCH_SHARE_GPU=1 (functional test of the N > 1 code path on a one-GPU
+# box, never a measurement): every rank uses device 0, the process group is
+# gloo, the dist handles run in lockstep (ranks sharing a GPU), no NCCL.
+SHARE_GPU = os.environ.get("SOR_BENCH_SHARE_GPU") == "1"
+
+
+def coll_dev():
+    """Device of tensors passed to torch.distributed collectives."""
+    return "cpu" if SHARE_GPU else "cuda"
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -352,7 +363,7 @@ def ipc_self_check(P, SI, make_grid, rank):
         if rank == 0:
             a, b = res["nccl"], res["ipc"]
             ok = int(np.array_equal(a[0], b[0]) and a[1:] == b[1:])
-        f = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        f = torch.tensor([ok], dtype=torch.int32, device=coll_dev())
         dist.broadcast(f, 0)
         return {"ok": bool(f.item()), "what": "iterate 61 + solve(1e-3) of a 1024^2 random field, T=4, "
                 "IPC vs NCCL, bitwise"}
@@ -380,7 +391,7 @@ def measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, p
         g.iterate(cfg.omega, cfg.iters)
         ms = g.elapsed_ms
         if world > 1:
-            tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([ms], dtype=torch.float64, device=coll_dev())
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = float(tt.item())
         ts.append(ms)
@@ -398,14 +409,16 @@ def measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, p
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f)
-        traffic = tr.get("C5:wave_kernel<f64,T=4,ck=0>", {}).get("dram_bytes_per_launch")
+        kfam = "wave2_kernel" if (world == 1 and os.environ.get("SOR_WAVE2", "1") != "0") else "wave_kernel"
+        traffic = tr.get(f"C5:{kfam}<f64,T=4,ck=0>", {}).get("dram_bytes_per_launch")
     return {"metric": "GLUP/s", "value": value, "unit": "GLUP/s", "ms": ms, "reps_ms": ts,
             "workload": f"C5: {cfg.rows}x{cfg.cols} f64, random edges seed 7, omega={cfg.omega!r}, "
                         f"{cfg.iters} iterations, T=4, median of {reps}",
             "n_gpus": world, "scaling": "strong",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                         "kernel": "wave_kernel<f64,T=4,ck=0>", "algorithmic_bytes_per_launch": bpl,
+                         "kernel": ("wave2_kernel" if (world == 1 and os.environ.get("SOR_WAVE2", "1") != "0")
+                                    else "wave_kernel") + "<f64,T=4,ck=0>", "algorithmic_bytes_per_launch": bpl,
                          "avg_launch_ms": t_launch, "peak_kind": pk_kind},
             "clocks": ck}
 
@@ -453,9 +466,14 @@ def main():
 
     rank, world, local = env_rank()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    if SHARE_GPU:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = SI.config(args.config, dtype=args.dtype)
     iters_fixed = cfg.iters
     do_solve = cfg.tol is not None and not args.no_solve
@@ -464,7 +482,7 @@ def main():
 
     def bcast_id(make):
         uid = make() if rank == 0 else bytes(128)
-        tb = torch.frombuffer(bytearray(uid), dtype=torch.uint8).cuda()
+        tb = torch.frombuffer(bytearray(uid), dtype=torch.uint8).to(coll_dev())
         dist.broadcast(tb, 0)
         return bytes(tb.cpu().numpy().tobytes())
 
@@ -479,7 +497,9 @@ def main():
                                   dtype=c.dtype, rows=c.rows, cols=c.cols)
 
     transport, transport_check = args.transport, None
-    if world > 1 and transport == "ipc":
+    if world > 1 and SHARE_GPU:
+        transport, transport_check = "ipc", {"ok": True, "what": "skipped: SOR_BENCH_SHARE_GPU test mode (no NCCL)"}
+    elif world > 1 and transport == "ipc":
         # the device-initiated path is checked against the NCCL path on this
         # node before it is timed (a short iterate + solve, bitwise); any
         # mismatch or error falls back to NCCL and says so in the JSON line
@@ -535,7 +555,7 @@ def main():
     ck = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
     if world > 1:
-        tt = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([ms_total], dtype=torch.float64, device=coll_dev())
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total = float(tt.item())
     iters_total = sum(r["iters"] for r in recs)
@@ -551,12 +571,14 @@ def main():
     t_it_total = sum(r["t_iterate_ms"] for r in recs)
     t_sv_total = sum(r["t_solve_ms"] for r in recs)
     solve_dominant = t_sv_total > t_it_total
+    # the skew-2 schedule (wave2_kernel) runs T >= 2 on one GPU unless SOR_WAVE2=0
+    kfam = "wave2_kernel" if (T_eff >= 2 and world == 1 and os.environ.get("SOR_WAVE2", "1") != "0") else "wave_kernel"
     if solve_dominant:
         t_launch_ms = t_sv_total / sum(r["solve_launches"] for r in recs)
-        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck={4 if T_eff > 1 else 1}> (solve phase)"
+        kname = f"{kfam}<{cfg.dtype},T={T_eff},ck={4 if T_eff > 1 else 1}> (solve phase)"
     else:
         t_launch_ms = t_it_total / sum(r["iterate_launches"] for r in recs)
-        kname = f"wave_kernel<{cfg.dtype},T={T_eff},ck=0> (fixed-iteration phase)"
+        kname = f"{kfam}<{cfg.dtype},T={T_eff},ck=0> (fixed-iteration phase)"
     rows_local = g.stats["row_hi"] - g.stats["row_lo"]
     bytes_per_launch = 2 * esz * rows_local * cfg.cols          # read X_{k0} + write X_{k0+T}, once each
     achieved = bytes_per_launch / (t_launch_ms * 1e-3) / 1e9
@@ -608,11 +630,13 @@ def main():
         "clocks": ck,
     }
 
-    # end-to-end through the C ABI with host buffers (H2D + D2H inside timing)
-    if not args.no_e2e and world == 1:
-        hin = torch.from_numpy(init_h).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
-        torch.cuda.synchronize()
+    # end-to-end through the C ABI with host buffers (H2D + D2H inside timing).
+    # N > 1: rank 0 passes the pinned host init (the library scatters the
+    # slabs) and receives the gathered grid; time = max over ranks.
+    if not args.no_e2e:
+        hin = torch.from_numpy(init_h).pin_memory() if rank == 0 else None
+        hout = torch.empty_like(hin).pin_memory() if rank == 0 else None
+        barrier()
         t0 = time.perf_counter()
         e_iters = 0
         for _ in range(args.steps):
@@ -623,7 +647,11 @@ def main():
                 e_iters += g.solve(cfg.omega, cfg.tol, cfg.maxit, cfg.check_every).iters
             g.download(hout)
         t = time.perf_counter() - t0
-        nbytes = hin.numel() * 8
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=coll_dev())
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        nbytes = init_h.size * 8
         line["e2e"] = {"value": cfg.rows * cfg.cols * e_iters / t / 1e9, "unit": "GLUP/s",
                        "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes}
     if transport_check is not None:

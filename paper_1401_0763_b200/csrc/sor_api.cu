@@ -1100,13 +1100,16 @@ bool wave_pdl(const sor_grid* g, unsigned blocks, int occ) {
   return !off && (single_part(g) || g->push) && !g->lockstep && blocks <= (unsigned)(occ * g->nsm);
 }
 
-// Skew-2 schedule of the wave kernel (wave2.cuh) for T >= 2: SOR_WAVE2=1
-// selects it (development: bitwise equal, A/B against the skew-1 schedule).
+// Skew-2 schedule of the wave kernel (wave2.cuh) for T >= 2 on single-slab
+// handles (bitwise equal; C3 T=4 iterate +3 %, C5 +3 %, T=2 +8 %:
+// profiles/r2_wave2_ab.txt).  SOR_WAVE2=0 selects the skew-1 schedule.
+// Pushing slabs (virtual, dist-IPC) keep the skew-1 kernel (its LINK
+// instances).
 bool use_wave2(const sor_grid* g, int T) {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("SOR_WAVE2");
-    on = e ? atoi(e) : 0;
+    on = e ? atoi(e) : 1;
   }
   return on != 0 && T >= 2 && !g->push;
 }

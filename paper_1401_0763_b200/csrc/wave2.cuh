@@ -56,8 +56,8 @@ struct WavePipe2 {
   static constexpr bool LANE_OWN = (2 * T) % NC == 0;
   static constexpr uint32_t ROWB = WC * sizeof(R);
   static constexpr int CH = 16 / (int)sizeof(R);
-  // CK 4 probes the red stages on rows with rel % 4 == 0 (static per step
-  // and stage: rel = t - 2s)
+  // CK 4 probes the red stages on rows with rel % 8 == 0: rel % 4 == 0 is
+  // static per step and stage (rel = t - 2s), the batch parity selects half
   __host__ __device__ static constexpr bool probe_row(int M, int s) { return (((M - 2 * s) % 4) + 4) % 4 == 0; }
   R F[4][NC];                 // source rows, slot = rel mod 4 (front warp)
   R C[S > 1 ? S - 1 : 1][4][NH];  // stage outputs, slot = step mod 4
@@ -169,6 +169,7 @@ struct WavePipe2 {
       }
     }
     if (CK == 4 && (s & 1) == 0 && probe_row(M, s)) {
+      if (pf)  // even batches only: probe rows with rel % 8 == 0
 #pragma unroll
       for (int h = 0; h < NH; ++h)
         hmax[s >> 1] = max(hmax[s >> 1], (unsigned int)hi_bits(rsub(v[h], u[h])) & ownM[h] & pf &
@@ -274,7 +275,9 @@ struct WavePipe2 {
 #pragma unroll 1
     for (int j = j0; j < j1; ++j) {
       const int t = kW2Batch * j;
-      if (CK == 4) pf = 0xffffffffu;  // ownership is tested per row in stage()
+      // CK 4: probe rows (rel % 8 == 0) only in even batches; ownership is
+      // tested per row in stage()
+      if (CK == 4) pf = (j & 1) ? 0u : 0xffffffffu;
       const R* rowp = nullptr;
       R* hp = split ? hand + (j & 1) * (kW2Batch * 32 * NC) : nullptr;
       if (front) {

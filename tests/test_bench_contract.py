@@ -47,3 +47,27 @@ def test_headline_line():
 def test_next_rows_lines(method):
     d = _run(["--method", method, "--steps", "2", "--warmup", "3", "--cpu-budget", "1"], 900)
     assert BASE_KEYS <= set(d) and d["value"] > 0 and d["roofline"]["frac"] > 0 and d["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_on_one_gpu():
+    """The N > 1 code path of bench.py (torchrun, dist-IPC handles, rank-0
+    scatter / gather, max over ranks) as a functional check on a one-GPU box:
+    SOR_BENCH_SHARE_GPU=1 puts both ranks on device 0 (lockstep, gloo); the
+    number it prints is not a measurement."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-c5", "--cpu-window", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env=dict(os.environ, SOR_BENCH_SHARE_GPU="1"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "ipc" in d["config"]["parallelism"]
+    assert d["config"]["solve_iterations"] == 12480 and d["e2e"]["value"] > 0

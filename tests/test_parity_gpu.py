@@ -212,7 +212,7 @@ def test_zero_iterations_and_stats(gpu):
         st = g.stats
         assert st["half_sweeps"] == 20 and st["hbm_passes"] == 3   # 2 + 4 + 4
         # the remainder pass, then both full passes in one persistent (K6) launch
-        assert st["kernel_launches"] == 2
+        assert st["kernel_launches"] == (3 if os.environ.get("SOR_NO_PERSIST") else 2)
         assert g.elapsed_ms > 0
 
 
