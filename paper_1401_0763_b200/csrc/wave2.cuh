@@ -20,12 +20,16 @@
 
 namespace sorb {
 
+#ifndef SOR_WAVE2_RING
+#define SOR_WAVE2_RING 3
+#endif
 constexpr int kW2Batch = 4;                  // steps (source rows) per TMA box / unrolled loop body
-constexpr int kW2Slots = 2 * kW2Batch + 3;   // ring: 2 batches + 3 prologue rows (rel -2, -1, 0)
+constexpr int kW2Ring = SOR_WAVE2_RING;      // source batches in flight (TMA look-ahead)
+constexpr int kW2Slots = kW2Ring * kW2Batch + 3;  // ring: kW2Ring batches + 3 prologue rows (rel -2, -1, 0)
 
 template <typename R, int NC>
 __host__ __device__ constexpr int wave2_smem_per_warp() {
-  return (kW2Slots * wave_cols<NC>() * (int)sizeof(R) + 3 * 8 + 127) / 128 * 128;
+  return (kW2Slots * wave_cols<NC>() * (int)sizeof(R) + (kW2Ring + 1) * 8 + 127) / 128 * 128;
 }
 template <typename R, int NC>
 __host__ __device__ constexpr int wave2_handoff_bytes() {
@@ -82,14 +86,15 @@ struct WavePipe2 {
   int bar_full, bar_empty;
 
   __device__ __forceinline__ void issue_batch_tma(int j) {
-    const uint32_t bar = bar_s + 8u * (j & 1);
+    const int b = j % kW2Ring;
+    const uint32_t bar = bar_s + 8u * b;
     mbar_expect_tx(bar, kW2Batch * ROWB);
-    tma_rows(ring_s + (j & 1) * kW2Batch * ROWB, tm, tm_x, tm_y + kW2Batch * j + 3, bar);  // rows rel 4j+1..4j+4
+    tma_rows(ring_s + b * kW2Batch * ROWB, tm, tm_x, tm_y + kW2Batch * j + 3, bar);  // rows rel 4j+1..4j+4
   }
   __device__ __forceinline__ void issue_prologue() {
-    const uint32_t bar = bar_s + 16u;
+    const uint32_t bar = bar_s + 8u * kW2Ring;
     mbar_expect_tx(bar, 3 * ROWB);
-    tma_rows(ring_s + 2 * kW2Batch * ROWB, tm3, tm_x, tm_y, bar);  // rows rel -2, -1, 0
+    tma_rows(ring_s + kW2Ring * kW2Batch * ROWB, tm3, tm_x, tm_y, bar);  // rows rel -2, -1, 0
   }
   __device__ __forceinline__ void ld_row(const R* row, R (&x)[NC]) { ldsN<NC>(row + NC * lane, x); }
   __device__ __forceinline__ void hand_st(R* hp, int M, const R (&x)[NC]) {
@@ -281,8 +286,9 @@ struct WavePipe2 {
       const R* rowp = nullptr;
       R* hp = split ? hand + (j & 1) * (kW2Batch * 32 * NC) : nullptr;
       if (front) {
-        mbar_wait(bar_s + 8u * (j & 1), (uint32_t)((j >> 1) & 1));
-        rowp = ring + (j & 1) * kW2Batch * WC;
+        const int b = j % kW2Ring;
+        mbar_wait(bar_s + 8u * b, (uint32_t)((j / kW2Ring) & 1));
+        rowp = ring + b * kW2Batch * WC;
         if (split) named_bar_sync(bar_empty + (j & 1), 64);
       } else {
         named_bar_sync(bar_full + (j & 1), 64);
@@ -291,7 +297,7 @@ struct WavePipe2 {
       if (front) {
         if (split) named_bar_arrive(bar_full + (j & 1), 64);
         __syncwarp();
-        if (lane == 0 && j + 2 < nbatch) issue_batch_tma(j + 2);
+        if (lane == 0 && j + kW2Ring < nbatch) issue_batch_tma(j + kW2Ring);
       } else if (j + 2 < nbatch) {
         named_bar_arrive(bar_empty + (j & 1), 64);
       }
@@ -376,17 +382,16 @@ __device__ __forceinline__ void wave2_tile(const WaveArgs<R>& a, const CUtensorM
   if (SB == 0) {
     if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) mbar_init(P.bar_s + 8u * k, 1u);
+      for (int k = 0; k < kW2Ring + 1; ++k) mbar_init(P.bar_s + 8u * k, 1u);
       mbar_fence_init();
     }
     __syncwarp();
     if (lane == 0) {
       P.issue_prologue();
-      P.issue_batch_tma(0);
-      if (P.nbatch > 1) P.issue_batch_tma(1);
+      for (int j = 0; j < kW2Ring && j < P.nbatch; ++j) P.issue_batch_tma(j);
     }
-    mbar_wait(P.bar_s + 16u, 0u);
-    const R* pro = P.ring + 2 * kW2Batch * WC;
+    mbar_wait(P.bar_s + 8u * kW2Ring, 0u);
+    const R* pro = P.ring + kW2Ring * kW2Batch * WC;
     P.ld_row(pro, P.F[2]);           // rel -2 -> slot 2
     P.ld_row(pro + WC, P.F[3]);      // rel -1 -> slot 3
     P.ld_row(pro + 2 * WC, P.F[0]);  // rel 0  -> slot 0
