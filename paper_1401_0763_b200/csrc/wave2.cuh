@@ -20,28 +20,27 @@
 
 namespace sorb {
 
-#ifndef SOR_WAVE2_RING
-#define SOR_WAVE2_RING 3
-#endif
-constexpr int kW2Batch = 4;                  // steps (source rows) per TMA box / unrolled loop body
-constexpr int kW2Ring = SOR_WAVE2_RING;      // source batches in flight (TMA look-ahead)
-constexpr int kW2Slots = kW2Ring * kW2Batch + 3;  // ring: kW2Ring batches + 3 prologue rows (rel -2, -1, 0)
+constexpr int kW2Batch = 4;  // steps (source rows) per TMA box / unrolled loop body
+// RING = source batches in flight (TMA look-ahead): 3 for one-wave launches
+// (C3: +3 %), 2 otherwise (C5, T < 4: the smaller footprint is faster)
+template <int RING>
+__host__ __device__ constexpr int wave2_slots() { return RING * kW2Batch + 3; }  // + 3 prologue rows (rel -2, -1, 0)
 
-template <typename R, int NC>
+template <typename R, int NC, int RING>
 __host__ __device__ constexpr int wave2_smem_per_warp() {
-  return (kW2Slots * wave_cols<NC>() * (int)sizeof(R) + (kW2Ring + 1) * 8 + 127) / 128 * 128;
+  return (wave2_slots<RING>() * wave_cols<NC>() * (int)sizeof(R) + (RING + 1) * 8 + 127) / 128 * 128;
 }
 template <typename R, int NC>
 __host__ __device__ constexpr int wave2_handoff_bytes() {
   return 2 * kW2Batch * 32 * NC * (int)sizeof(R);  // 2 batches x 4 steps x 32 lanes x NC values
 }
-template <typename R, int NC>
+template <typename R, int NC, int RING>
 __host__ __device__ constexpr int wave2_smem_per_pair() {
-  return wave2_smem_per_warp<R, NC>() + wave2_handoff_bytes<R, NC>();
+  return wave2_smem_per_warp<R, NC, RING>() + wave2_handoff_bytes<R, NC>();
 }
-template <typename R, bool SPLIT, int NC>
+template <typename R, bool SPLIT, int NC, int RING>
 __host__ __device__ constexpr int wave2_smem_bytes() {
-  return SPLIT ? (kWaveWarps / 2) * wave2_smem_per_pair<R, NC>() : kWaveWarps * wave2_smem_per_warp<R, NC>();
+  return SPLIT ? (kWaveWarps / 2) * wave2_smem_per_pair<R, NC, RING>() : kWaveWarps * wave2_smem_per_warp<R, NC, RING>();
 }
 #ifndef SOR_WAVE2_K4
 #define SOR_WAVE2_K4 3
@@ -51,8 +50,9 @@ __host__ __device__ constexpr int wave2_split_stage(int T) { return T == 4 ? SOR
 // Warp pipeline: stages [SB, SE) of S = 2T.  Step t (relative to the tile's
 // first front row i_first, even): the front row is rel t; stage s updates row
 // rel t-2s, colour s&1, cells q = O + 2h with O = (s + t) & 1.
-template <typename R, int T, int CK, int SB, int SE, int NC>
+template <typename R, int T, int CK, int SB, int SE, int NC, int RING>
 struct WavePipe2 {
+  static constexpr int kW2Ring = RING;
   static constexpr int S = 2 * T;
   static constexpr int NH = NC / 2;
   static constexpr int WC = wave_cols<NC>();
@@ -326,11 +326,12 @@ struct WavePipe2 {
   }
 };
 
-template <typename R, int T, int CK, int SB, int SE, int NC>
+template <typename R, int T, int CK, int SB, int SE, int NC, int RING>
 __device__ __forceinline__ void wave2_tile(const WaveArgs<R>& a, const CUtensorMap* tm4, const CUtensorMap* tm3,
                                            unsigned char* wbase, R* hand, int bar_id, int lane, int sw, int R0, int R1,
                                            int i_first, int nsteps, unsigned long long (&dm)[kMaxT]) {
-  using Pipe = WavePipe2<R, T, CK, SB, SE, NC>;
+  using Pipe = WavePipe2<R, T, CK, SB, SE, NC, RING>;
+  constexpr int kW2Ring = RING;
   constexpr int WC = Pipe::WC, NH = Pipe::NH;
   Pipe P;
 #pragma unroll
@@ -340,7 +341,7 @@ __device__ __forceinline__ void wave2_tile(const WaveArgs<R>& a, const CUtensorM
   }
   P.ring = reinterpret_cast<const R*>(wbase);
   P.ring_s = smem_u32(wbase);
-  P.bar_s = P.ring_s + kW2Slots * WC * sizeof(R);
+  P.bar_s = P.ring_s + wave2_slots<RING>() * WC * sizeof(R);
   P.hand = hand;
   P.bar_full = bar_id;
   P.bar_empty = bar_id + 2;
@@ -405,7 +406,7 @@ __device__ __forceinline__ void wave2_tile(const WaveArgs<R>& a, const CUtensorM
 // The kernel: wave_kernel's launch protocol (PDL, stop test, deferred
 // decision, max reduction) around wave2_tile.  Tensor maps: m[0] 4-row and
 // m[1] 3-row boxes (wave2 maps of the source plane).
-template <typename R, int T, int CK, bool SPLIT, int NC, bool LINK>
+template <typename R, int T, int CK, bool SPLIT, int NC, bool LINK, int RING>
 __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
     wave2_kernel(WaveArgs<R> a, IterCtl ctl, const __grid_constant__ WaveMaps tm) {
   const int bid = (int)blockIdx.x - ctl.defer;
@@ -440,19 +441,19 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
     const int nsteps = (R1 - i_first + 2 * (2 * T - 1) + kW2Batch - 1) / kW2Batch * kW2Batch;
     if (LINK && role == 0) tile_halo_wait(a, sw, WC, R0, R1, 2 * T, lane, ctl.st);
     if (SPLIT) {
-      unsigned char* pbase = wave_smem + slot * wave2_smem_per_pair<R, NC>();
-      R* hand = reinterpret_cast<R*>(pbase + wave2_smem_per_warp<R, NC>());
+      unsigned char* pbase = wave_smem + slot * wave2_smem_per_pair<R, NC, RING>();
+      R* hand = reinterpret_cast<R*>(pbase + wave2_smem_per_warp<R, NC, RING>());
       const int bar_id = 1 + 4 * slot;
       constexpr int K = wave2_split_stage(T);
       if (role == 0)
-        wave2_tile<R, T, CK, 0, K, NC>(a, &tm.m[0], &tm.m[1], pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps,
+        wave2_tile<R, T, CK, 0, K, NC, RING>(a, &tm.m[0], &tm.m[1], pbase, hand, bar_id, lane, sw, R0, R1, i_first, nsteps,
                                        dm);
       else
-        wave2_tile<R, T, CK, K, 2 * T, NC>(a, &tm.m[0], &tm.m[1], pbase, hand, bar_id, lane, sw, R0, R1, i_first,
+        wave2_tile<R, T, CK, K, 2 * T, NC, RING>(a, &tm.m[0], &tm.m[1], pbase, hand, bar_id, lane, sw, R0, R1, i_first,
                                            nsteps, dm);
     } else {
-      unsigned char* wbase = wave_smem + warp * wave2_smem_per_warp<R, NC>();
-      wave2_tile<R, T, CK, 0, 2 * T, NC>(a, &tm.m[0], &tm.m[1], wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps,
+      unsigned char* wbase = wave_smem + warp * wave2_smem_per_warp<R, NC, RING>();
+      wave2_tile<R, T, CK, 0, 2 * T, NC, RING>(a, &tm.m[0], &tm.m[1], wbase, nullptr, 0, lane, sw, R0, R1, i_first, nsteps,
                                          dm);
     }
   }
@@ -485,6 +486,63 @@ __global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC)
       }
       maybe_finalize(ctl);
     }
+  }
+}
+
+// K6 with the skew-2 tiles: `npasses` T-deep passes in one cooperative
+// launch, grid barrier between passes (see wave_persist_kernel).
+template <typename R, int T, bool SPLIT, int NC>
+__global__ void __launch_bounds__(kWaveWarps * 32, wave_min_blocks(T, SPLIT, NC))
+    wave2_persist_kernel(WaveArgs<R> a, int npasses, unsigned* gbar, const __grid_constant__ WaveMaps tmA,
+                         const __grid_constant__ WaveMaps tmB) {
+  constexpr int RING = 2;
+  extern __shared__ __align__(128) unsigned char wave_smem[];
+  constexpr int WC = wave_cols<NC>();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int slot = SPLIT ? warp >> 1 : warp;
+  const int role = SPLIT ? warp & 1 : 0;
+  const int gw = (int)blockIdx.x * wave_tiles_per_cta(SPLIT) + slot;
+  const bool has_tile = gw < a.ntiles;
+  const int4 tile = has_tile ? a.tiles[gw] : make_int4(0, 0, 0, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  unsigned long long dm[kMaxT] = {};
+  for (int p = 0; p < npasses; ++p) {
+    WaveArgs<R> ap = a;
+    if (p & 1) {
+      ap.src = a.dst;
+      ap.dst = const_cast<R*>(a.src);
+    }
+    const CUtensorMap* tm = (p & 1) ? tmB.m : tmA.m;
+    if (has_tile) {
+      const int sw = a.s0 + tile.x * (WC - 4 * T);
+      const int R0 = tile.y, R1 = tile.z;
+      const int i_first = (R0 - (2 * T - 1)) & ~1;
+      const int nsteps = (R1 - i_first + 2 * (2 * T - 1) + kW2Batch - 1) / kW2Batch * kW2Batch;
+      unsigned char* base = SPLIT ? wave_smem + slot * wave2_smem_per_pair<R, NC, RING>()
+                                  : wave_smem + warp * wave2_smem_per_warp<R, NC, RING>();
+      if (SPLIT) {
+        R* hand = reinterpret_cast<R*>(base + wave2_smem_per_warp<R, NC, RING>());
+        const int bar_id = 1 + 4 * slot;
+        constexpr int K = wave2_split_stage(T);
+        if (role == 0)
+          wave2_tile<R, T, 0, 0, K, NC, RING>(ap, &tm[0], &tm[1], base, hand, bar_id, lane, sw, R0, R1, i_first, nsteps,
+                                              dm);
+        else
+          wave2_tile<R, T, 0, K, 2 * T, NC, RING>(ap, &tm[0], &tm[1], base, hand, bar_id, lane, sw, R0, R1, i_first,
+                                                  nsteps, dm);
+      } else {
+        wave2_tile<R, T, 0, 0, 2 * T, NC, RING>(ap, &tm[0], &tm[1], base, nullptr, 0, lane, sw, R0, R1, i_first, nsteps,
+                                                dm);
+      }
+      if (role == 0 && lane == 0) {
+        const uint32_t bar = smem_u32(base) + wave2_slots<RING>() * WC * (uint32_t)sizeof(R);
+#pragma unroll
+        for (int k = 0; k < RING + 1; ++k) mbar_inval(bar + 8u * k);
+      }
+    }
+    if (p + 1 < npasses) grid_barrier(gbar, (unsigned)(p + 1) * gridDim.x);
   }
 }
 

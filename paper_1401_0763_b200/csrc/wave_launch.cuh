@@ -62,18 +62,18 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
 }
 
 // The skew-2 schedule (wave2.cuh): the same tiles and launch protocol.
-template <typename R, int T, int CK, bool LINK>
-int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+template <typename R, int T, int CK, bool LINK, int RING>
+int launch_wave2_TR(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
   constexpr bool SPLIT = T >= 2;
   constexpr int NC = kWaveNC;
-  constexpr int smem = wave2_smem_bytes<R, SPLIT, NC>();
+  constexpr int smem = wave2_smem_bytes<R, SPLIT, NC, RING>();
   constexpr int per_cta = wave_tiles_per_cta(SPLIT);
   static int occ_dev[kMaxDev] = {};
   int& occ = occ_dev[g->device % kMaxDev];
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave2_kernel<R, T, CK, SPLIT, NC, LINK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(wave2_kernel<R, T, CK, SPLIT, NC, LINK, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave2_kernel<R, T, CK, SPLIT, NC, LINK>, kWaveWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave2_kernel<R, T, CK, SPLIT, NC, LINK, RING>, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -108,9 +108,18 @@ int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, wave2_kernel<R, T, CK, SPLIT, NC, LINK>, a, c, s.tmap2[g->cur]));
+  CU(cudaLaunchKernelEx(&cfg, wave2_kernel<R, T, CK, SPLIT, NC, LINK, RING>, a, c, s.tmap2[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
+}
+
+template <typename R, int T, int CK, bool LINK>
+int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin) {
+  // a deeper TMA look-ahead pays for one-wave launches at T = 4 (C3-sized
+  // slabs); multi-wave launches (C4, C5) and T < 4 keep the smaller ring
+  const double cells = (double)(s.g_hi - s.g_lo) * (double)g->cols;
+  if (T == 4 && cells <= 64.0 * (1 << 20)) return launch_wave2_TR<R, T, CK, LINK, 3>(g, s, w, ctl, fused_fin);
+  return launch_wave2_TR<R, T, CK, LINK, 2>(g, s, w, ctl, fused_fin);
 }
 
 template <typename R, int T, int CK, bool LINK>
@@ -124,20 +133,19 @@ int launch_wave_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fuse
 // K6: `npasses` T-deep passes in one cooperative launch (L2-resident grids;
 // see wave_persist_kernel).  Returns SOR_E_UNSUPPORTED if the tiles do not fit
 // in one wave of co-resident CTAs (the caller then launches pass by pass).
-template <typename R, int T>
-int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar) {
+template <typename R, int T, bool W2>
+int launch_wave_persist_S(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar) {
   constexpr int NST = wave_nst<R>();
   constexpr bool SPLIT = T >= 2;
   constexpr int NC = kWaveNC;
-  constexpr int smem = wave_smem_bytes<R, NST, SPLIT, NC>();
+  constexpr int smem = W2 ? wave2_smem_bytes<R, SPLIT, NC, 2>() : wave_smem_bytes<R, NST, SPLIT, NC>();
+  auto kern = W2 ? wave2_persist_kernel<R, T, SPLIT, NC> : wave_persist_kernel<R, T, NST, SPLIT, NC>;
   constexpr int per_cta = wave_tiles_per_cta(SPLIT);
   static int occ_dev[kMaxDev] = {};
   int& occ = occ_dev[g->device % kMaxDev];
   if (occ == 0) {
-    CU(cudaFuncSetAttribute(wave_persist_kernel<R, T, NST, SPLIT, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave_persist_kernel<R, T, NST, SPLIT, NC>, kWaveWarps * 32,
-                                                  smem);
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWaveWarps * 32, smem);
     if (occ <= 0) occ = 1;
   }
   WaveArgs<R> a;
@@ -181,9 +189,20 @@ int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* 
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CU(cudaLaunchKernelEx(&cfg, wave_persist_kernel<R, T, NST, SPLIT, NC>, a, npasses, gbar, s.tmap[p0], s.tmap[p1]));
+  if (W2)
+    CU(cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap2[p0], s.tmap2[p1]));
+  else
+    CU(cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap[p0], s.tmap[p1]));
   g->st.kernel_launches += 1;
   return SOR_OK;
+}
+
+template <typename R, int T>
+int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* gbar) {
+  if constexpr (T >= 2) {
+    if (use_wave2(g, T)) return launch_wave_persist_S<R, T, true>(g, s, w, npasses, gbar);
+  }
+  return launch_wave_persist_S<R, T, false>(g, s, w, npasses, gbar);
 }
 
 // Jacobi pass (NEXT-2): jacobi_kernel on the wave tiles with ghost G and T stages.
