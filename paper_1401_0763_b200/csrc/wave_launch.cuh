@@ -55,7 +55,8 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   // PDL only for one-wave launches (wave_pdl)
-  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  // the deferred decision block (block 0) exits at once: still one wave
+  cfg.numAttrs = wave_pdl(g, blocks - (ctl.defer ? 1u : 0u), occ) ? 1 : 0;
   CU(cudaLaunchKernelEx(&cfg, wave_kernel<R, T, NST, CK, SPLIT, NC, LINK>, a, c, s.tmap[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
@@ -107,7 +108,8 @@ int launch_wave2_TR(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fu
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  // the deferred decision block (block 0) exits at once: still one wave
+  cfg.numAttrs = wave_pdl(g, blocks - (ctl.defer ? 1u : 0u), occ) ? 1 : 0;
   CU(cudaLaunchKernelEx(&cfg, wave2_kernel<R, T, CK, SPLIT, NC, LINK, RING>, a, c, s.tmap2[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
@@ -249,7 +251,8 @@ int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_f
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = wave_pdl(g, blocks, occ) ? 1 : 0;
+  // the deferred decision block (block 0) exits at once: still one wave
+  cfg.numAttrs = wave_pdl(g, blocks - (ctl.defer ? 1u : 0u), occ) ? 1 : 0;
   CU(cudaLaunchKernelEx(&cfg, jacobi_kernel<R, T, NST, CK, LINK>, a, c, s.tmap[g->cur]));
   g->st.kernel_launches += 1;
   return SOR_OK;
