@@ -1876,6 +1876,9 @@ int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
       const size_t bytes = (size_t)(g->rows + 2) * (g->cols + 2) * g->esz;
       if (bytes > k5_limit_bytes())
         return set_error(nullptr, SOR_E_UNSUPPORTED, "grid of %zu bytes exceeds shared memory", bytes);
+      if (g->rows * ((g->cols + 1) / 2) > (int64_t)kK5Cells * 1024)
+        return set_error(nullptr, SOR_E_UNSUPPORTED, "grid has more than %d cells of one colour for K5",
+                         kK5Cells * 1024);
       g->kernel = kernel;
       g->tdepth = 1;
       break;

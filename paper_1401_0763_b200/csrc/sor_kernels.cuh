@@ -1809,6 +1809,8 @@ __global__ void __launch_bounds__(K3Geo<KX, KY>::NT)
 // Whole grid (rows+2) x (cols+2) in shared memory; Algorithm 1's loop on one
 // CTA.  __syncthreads() is the phase barrier [P:314, P:317].  Used for small
 // grids (BJ configs[0]) where launch latency dominates.
+constexpr int kK5Cells = 13;  // cells of one colour per thread (1024 threads; <= 200 KB grids)
+
 template <typename R>
 __global__ void __launch_bounds__(1024) k5_small_solve(R* base, long long pitch, long long g0,
                                                        int rows, int cols, R w, int solve,
@@ -1823,54 +1825,75 @@ __global__ void __launch_bounds__(1024) k5_small_solve(R* base, long long pitch,
     const int i = c / ld, j = c % ld;
     u[c] = base[(i - g0) * pitch + j];
   }
-  __shared__ unsigned long long red[32];
-  __shared__ int s_stop;
-  if (threadIdx.x == 0) s_stop = 0;
-  __syncthreads();
+  // each thread's cells of each colour, as shared-memory offsets (-1: none),
+  // computed once (Code 2's stride-2 enumeration)
   const int half = (cols + 1) / 2;  // max cells of one colour per row
   const int per_phase = rows * half;
-  long long k = 1;
+  int off[2][kK5Cells];
+#pragma unroll
+  for (int color = 0; color < 2; ++color)
+#pragma unroll
+    for (int k = 0; k < kK5Cells; ++k) {
+      const int c = (int)threadIdx.x + k * (int)blockDim.x;
+      off[color][k] = -1;
+      if (c < per_phase) {
+        const int i = 1 + c / half;
+        const int j = ((((i + 1) & 1) == color) ? 1 : 2) + 2 * (c % half);
+        if (j <= cols) off[color][k] = i * ld + j;
+      }
+    }
+  // per-warp maxima, double-buffered by iteration parity: iteration k writes
+  // slot k&1 and every thread reads all of it after the barrier, so no
+  // barrier is needed before the next check overwrites the other slot
+  __shared__ unsigned long long wmax[2][32];
+  __syncthreads();
+  long long k = 1, checks = 0;
+  double last = 0.0;
+  int converged = 0;
   for (; k <= n_iter; ++k) {
     const int check = solve ? (k % K == 0) : (measure_last && k == n_iter);
     unsigned long long dmax = 0ull;
+#pragma unroll
     for (int color = 0; color < 2; ++color) {
-      for (int c = threadIdx.x; c < per_phase; c += blockDim.x) {
-        const int i = 1 + c / half;
-        const int j = ((((i + 1) & 1) == color) ? 1 : 2) + 2 * (c % half);
-        if (j <= cols) {
-          R* uc = u + i * ld;
-          const R uo = uc[j];
-          const R un = sor_update(radd(uc[j - ld], uc[j + ld]), radd(uc[j - 1], uc[j + 1]), uo, w);
+#pragma unroll
+      for (int q = 0; q < kK5Cells; ++q) {
+        const int o = off[color][q];
+        if (o >= 0) {
+          const R uo = u[o];
+          const R un = sor_update(radd(u[o - ld], u[o + ld]), radd(u[o - 1], u[o + 1]), uo, w);
           if (check) dmax = umax64(dmax, delta_bits(un, uo));
-          uc[j] = un;
+          u[o] = un;
         }
       }
-      __syncthreads();
+      __syncthreads();  // the phase barrier [P:314, P:317]
     }
     if (check) {
       dmax = warp_max_u64(dmax);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+      if ((threadIdx.x & 31) == 0) wmax[k & 1][threadIdx.x >> 5] = dmax;
       __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long m = 0ull;
-        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = umax64(m, red[q]);
-        const double md = __longlong_as_double((long long)m);
-        st->checks += 1;
-        st->max_change = md;
-        if (solve && md < tol) {
-          st->converged = 1;
-          st->conv_iter = k;
-          s_stop = 1;
-        }
+      // every warp folds the warp maxima lane-parallel (one load per lane)
+      const int lane = threadIdx.x & 31;
+      unsigned long long m = lane < (int)(blockDim.x >> 5) ? wmax[k & 1][lane] : 0ull;
+      m = warp_max_u64(m);
+      last = __longlong_as_double((long long)m);
+      ++checks;
+      if (solve && last < tol) {  // every thread decides the same (strict <)
+        converged = 1;
+        break;
       }
-      __syncthreads();
-      if (s_stop) break;
     }
   }
   if (threadIdx.x == 0) {
+    st->checks += checks;
+    if (checks) st->max_change = last;
+    if (converged) {
+      st->converged = 1;
+      st->conv_iter = k;
+    }
     st->iters_done = k > n_iter ? n_iter : k;
     st->stop = 1;
   }
+  __syncthreads();
   for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
     const int i = c / ld, j = c % ld;
     base[(i - g0) * pitch + j] = u[c];

@@ -314,3 +314,21 @@ def test_fallback_paths_in_subprocess(gpu, env):
     e = dict(os.environ, **{env: "1"})
     r = subprocess.run([sys.executable, "-c", _SUBPROC % root], env=e, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("rows,cols", [(1, 1), (3, 5), (31, 33), (64, 64), (100, 120), (90, 130)])
+def test_small_kernel_iterate_and_solve(gpu, orc, dtype, rows, cols):
+    """K5 (whole grid in one CTA's shared memory, every iteration and the stop
+    test in one launch) on odd, ragged and degenerate shapes."""
+    init = _field(rows, cols, seed=rows * 7 + cols, dtype=dtype)
+    ref, rep = _oracle_iterate(orc, init, dtype, 1.6, 13, measure_last=True)
+    with gpu.Grid.create(init, dtype=dtype) as g:
+        g.set_kernel("small")
+        d = g.iterate(1.6, 13, want_delta=True)
+        assert np.array_equal(g.download(), ref) and d == rep.max_change
+        u = orc.to_storage(ref, dtype)
+        rr = orc.solve(u, 1.9, 1e-5, 600, 3)
+        r = g.solve(1.9, 1e-5, 600, 3)
+        assert (r.converged, r.iters, r.max_change) == (rr.status == 0, rr.iters, rr.max_change)
+        assert np.array_equal(g.download(), u.astype(np.float64))
