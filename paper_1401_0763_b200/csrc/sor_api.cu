@@ -949,8 +949,9 @@ static bool tile_masked(const sor_grid* g, int ghost, int S, int wc, int s0, int
 }
 
 int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int wc, int tiles_per_sm, bool split,
-               int s0, std::pair<int4*, int>* out) {
-  const auto key = std::make_tuple(slab_idx, ((ghost * 16 + S) * 2 + (split ? 1 : 0)) * 1024 + wc, tiles_per_sm);
+               int s0, std::pair<int4*, int>* out, int reserve) {
+  const auto key =
+      std::make_tuple(slab_idx, ((ghost * 16 + S) * 2 + (split ? 1 : 0)) * 1024 + wc, tiles_per_sm * 64 + reserve);
   auto it = g->tiles.find(key);
   if (it != g->tiles.end()) {
     *out = it->second;
@@ -973,7 +974,7 @@ int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int w
   const int64_t wout = wc - 2 * ghost;
   const int nstrips = (int)((g->cols + 1 - (s0 + ghost) + wout - 1) / wout);
   const int64_t nrows = s.g_hi - s.g_lo;
-  const int64_t slots = (int64_t)g->nsm * tiles_per_sm;
+  const int64_t slots = (int64_t)g->nsm * tiles_per_sm - reserve;
   const int64_t warm = 2 * (S - 1);
   // split strip `w` given the target cost per tile (in row-steps)
   auto split_strip = [&](int w, double cost, std::vector<int4>* tl) {

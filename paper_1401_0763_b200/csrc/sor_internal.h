@@ -168,8 +168,10 @@ bool host_all_finite(const double* p, int64_t n);
 
 // Wave-kernel tiles of slab `s` for a layout (ghost columns per side, S stages,
 // strip width wc, tiles per SM, split pairs, strip origin s0); cached.
+// `reserve` tiles of the one-wave budget are left free (the deferred stop
+// test's decision CTA).
 int wave_tiles(sor_grid* g, const Slab& s, int slab_idx, int ghost, int S, int wc, int tiles_per_sm, bool split,
-               int s0, std::pair<int4*, int>* out);
+               int s0, std::pair<int4*, int>* out, int reserve = 0);
 bool wave_pdl(const sor_grid* g, unsigned blocks, int occ);
 // HaloLink of slab `s` for a pass src -> dst with the given strip layout; also
 // records the layout as the writer of plane dst.

@@ -36,7 +36,8 @@ int launch_wave_TS(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   a.s0 = -4 * ((2 * T + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt,
+                 ctl.defer ? per_cta : 0));
   a.tiles = tt.first;
   a.ntiles = tt.second;
   a.link = make_link(g, s, g->cur, g->nxt(g->cur));
@@ -90,7 +91,8 @@ int launch_wave2_TR(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fu
   a.s0 = -4 * ((2 * T + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, 2 * T, 2 * T, wave_cols<NC>(), occ * per_cta, SPLIT, a.s0, &tt,
+                 ctl.defer ? per_cta : 0));
   a.tiles = tt.first;
   a.ntiles = tt.second;
   a.link = make_link(g, s, g->cur, g->nxt(g->cur));
@@ -233,7 +235,8 @@ int launch_jacobi_T(sor_grid* g, const Slab& s, const IterCtl& ctl, bool fused_f
   a.s0 = -4 * ((G + 3) / 4);
   const int slab_idx = (int)(&s - &g->slabs[0]);
   std::pair<int4*, int> tt{nullptr, 0};
-  TRY(wave_tiles(g, s, slab_idx, G, T, wave_cols<kWaveNC>(), occ * kWaveWarps, false, a.s0, &tt));
+  TRY(wave_tiles(g, s, slab_idx, G, T, wave_cols<kWaveNC>(), occ * kWaveWarps, false, a.s0, &tt,
+                 ctl.defer ? kWaveWarps : 0));
   a.tiles = tt.first;
   a.ntiles = tt.second;
   a.link = make_link(g, s, g->cur, g->nxt(g->cur));
