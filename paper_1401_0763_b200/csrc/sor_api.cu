@@ -650,7 +650,14 @@ int ipc_connect(sor_grid* g, const char* id) {
   CU(cudaMalloc(&g->djoin, sizeof(DistJoinTab)));
   CU(cudaMemcpyAsync(g->djoin, &tab, sizeof tab, cudaMemcpyHostToDevice, g->stream));
   CU(cudaStreamSynchronize(g->stream));
-  return shm_barrier(g);
+  TRY(shm_barrier(g));
+  // every rank has mapped the segment: drop its name now, so the id can
+  // rendezvous the next handle at once (the mapping stays valid)
+  if (g->shm->owner) {
+    shm_unlink(g->shm->name.c_str());
+    g->shm->owner = false;
+  }
+  return SOR_OK;
 }
 
 // Rank 0 writes every rank's planes through the IPC mappings; the barrier

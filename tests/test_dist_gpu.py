@@ -142,3 +142,15 @@ def test_dist_ipc_processes(gpu, nranks):
     assert "DONE fails=0" in log, log + "\n" + "\n".join(o[1][-2000:] for o in outs)
     assert all(p.returncode == 0 for p in procs), [o[1][-2000:] for o in outs]
     assert log.count("ok  ") >= 25
+
+
+@pytest.mark.parametrize("nranks,seed", [(2, 41), (3, 42)])
+def test_dist_ipc_random_sequences(gpu, nranks, seed):
+    """Random collective call sequences on dist-IPC handles (shapes, dtypes,
+    depths, SOR/Jacobi, iterate/solve/reset/download_rows), every rank a
+    process on the one GPU, rank 0 bitwise against the oracle
+    (tools/fuzz_dist_ipc.py)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_dist_ipc.py"), "launch", str(nranks), "12",
+                        str(seed)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 bad" in r.stdout, r.stdout[-3000:]
