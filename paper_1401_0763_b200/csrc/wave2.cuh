@@ -45,9 +45,6 @@ __host__ __device__ constexpr int wave2_smem_bytes() {
 #ifndef SOR_WAVE2_K4
 #define SOR_WAVE2_K4 3
 #endif
-#ifndef SOR_WAVE2_SKIP
-#define SOR_WAVE2_SKIP 1
-#endif
 __host__ __device__ constexpr int wave2_split_stage(int T) { return T == 4 ? SOR_WAVE2_K4 : T; }
 
 // Warp pipeline: stages [SB, SE) of S = 2T.  Step t (relative to the tile's
@@ -131,24 +128,8 @@ struct WavePipe2 {
 
   // One stage at step t = 4j + M: row rel t - 2s.  `uext` (stage SB of the back
   // warp) is the old value handed over by the front warp.
-  // A stage-row outside the dependency cone of the tile's owned rows [R0, R1)
-  // (stage s needs rows R0-(S-1-s) .. R1-1+(S-1-s)) reaches no owned result:
-  // it is skipped (warp-uniform), which saves the FP64 work of the pipeline
-  // fill and drain (about 3 stage-rows per stage at each band end).
   template <int MK, int M, int s>
   __device__ __forceinline__ void stage(const WaveArgs<R>& a, int t, const R* uext) {
-#if SOR_WAVE2_SKIP
-    const int r = i_first + t - 2 * s;
-    if (r < R0 - (S - 1 - s) || r > R1 - 1 + (S - 1 - s)) {
-      if (s == S - 1) orow += pitch;
-      return;
-    }
-#endif
-    stage_body<MK, M, s>(a, t, uext);
-  }
-
-  template <int MK, int M, int s>
-  __device__ __forceinline__ void stage_body(const WaveArgs<R>& a, int t, const R* uext) {
     constexpr int O = (s + M) & 1;
     constexpr int Q1 = (M + 3) & 3;  // slot of step t-1
     constexpr int Q2 = (M + 2) & 3;  // t-2
