@@ -147,7 +147,15 @@ int shm_open_seg(sor_grid* g, const char* id, int rank, int nranks) {
       usleep(1000);
     }
     struct stat stt{};
-    while (fstat(fd, &stt) == 0 && (size_t)stt.st_size < sizeof(ShmHdr)) usleep(1000);
+    const auto t1 = std::chrono::steady_clock::now();
+    while (fstat(fd, &stt) == 0 && (size_t)stt.st_size < sizeof(ShmHdr)) {
+      if (std::chrono::steady_clock::now() - t1 > std::chrono::seconds(120)) {
+        close(fd);
+        delete s;
+        return set_error(nullptr, SOR_E_STATE, "dist-ipc: rank %d: segment %s never sized", rank, name);
+      }
+      usleep(1000);
+    }
   }
   void* p = mmap(nullptr, sizeof(ShmHdr), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   close(fd);
