@@ -68,7 +68,9 @@ typedef enum {
   SOR_KERNEL_NATURAL = 1,  /* K1: one launch per colour phase, in place, natural layout */
   SOR_KERNEL_FUSED = 3,    /* K3: red+black fused in one HBM pass, src->dst ping-pong  */
   SOR_KERNEL_TEMPORAL = 4, /* K4: T iterations per HBM pass (temporal blocking)         */
-  SOR_KERNEL_SMALL = 5     /* K5: whole grid in one CTA's shared memory, one launch     */
+  SOR_KERNEL_SMALL = 5,    /* K5: whole grid in one CTA (registers if <= 126 columns,   */
+                           /*     else shared memory), one launch                        */
+  SOR_KERNEL_RESIDENT = 6  /* K7: grid register-resident across the SMs, one CTA per SM  */
 } sor_kernel;
 
 /* Create a single-GPU handle on the current CUDA device.
@@ -129,10 +131,19 @@ int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double*
                        sor_dtype dt, int nslabs);
 
 /* Select the kernel variant.  temporal_depth T (iterations per HBM pass) is
- * used by SOR_KERNEL_TEMPORAL only, 1 <= T <= SOR_MAX_T (T = 1 equals FUSED;
- * multi-slab grids need slabs of >= 2T rows).  SOR_KERNEL_SMALL requires a
- * single-slab grid that fits in shared memory; SOR_KERNEL_NATURAL is not
- * available on dist-IPC handles (SOR_E_UNSUPPORTED).
+ * used by SOR_KERNEL_TEMPORAL and SOR_KERNEL_RESIDENT, 1 <= T <= SOR_MAX_T
+ * (T = 1 equals FUSED; multi-slab grids need slabs of >= 2T rows).
+ * SOR_KERNEL_SMALL requires a single-slab grid that fits in shared memory;
+ * SOR_KERNEL_NATURAL is not available on dist-IPC handles (SOR_E_UNSUPPORTED).
+ * SOR_KERNEL_RESIDENT (K7, for small grids; the paper's per-phase barrier
+ * [P:203, P:314, P:317] becomes a CTA barrier and neighbour-only flags):
+ * sor_iterate on a single-slab grid that fits one 2-D block per SM (window of
+ * block + 2T ring <= 128 columns x ~80-90 rows: up to ~1.2 M cells) runs all
+ * its passes of T iterations in one cooperative launch, blocks exchanging only
+ * the 2T-deep frames with their 8 neighbours between passes; a grid of at most
+ * 126 columns and ~94 rows runs (iterate and solve) on one CTA with the stop
+ * test on the device.  Anything else runs as SOR_KERNEL_TEMPORAL with depth T.
+ * Jacobi calls run as SOR_KERNEL_TEMPORAL.
  * Returns SOR_E_INVAL / SOR_E_UNSUPPORTED without changing the handle.      */
 int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth);
 

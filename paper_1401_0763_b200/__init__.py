@@ -22,9 +22,10 @@ from .build import LIB, build_lib
 SOR_OK, SOR_NOT_CONVERGED = 0, 1
 SOR_E_INVAL, SOR_E_NOMEM, SOR_E_CUDA, SOR_E_NCCL, SOR_E_STATE, SOR_E_UNSUPPORTED = -1, -2, -3, -4, -5, -6
 F64, F32 = 0, 1
-KERNEL_NATURAL, KERNEL_FUSED, KERNEL_TEMPORAL, KERNEL_SMALL = 1, 3, 4, 5
+KERNEL_NATURAL, KERNEL_FUSED, KERNEL_TEMPORAL, KERNEL_SMALL, KERNEL_RESIDENT = 1, 3, 4, 5, 6
 KERNELS = {"natural": KERNEL_NATURAL, "k1": KERNEL_NATURAL, "fused": KERNEL_FUSED, "k3": KERNEL_FUSED,
-           "temporal": KERNEL_TEMPORAL, "k4": KERNEL_TEMPORAL, "small": KERNEL_SMALL, "k5": KERNEL_SMALL}
+           "temporal": KERNEL_TEMPORAL, "k4": KERNEL_TEMPORAL, "small": KERNEL_SMALL, "k5": KERNEL_SMALL,
+           "resident": KERNEL_RESIDENT, "k7": KERNEL_RESIDENT}
 
 EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_id",
            "sor_create_dist_ipc", "sor_ipc_unique_id",

@@ -415,6 +415,7 @@ void free_grid(sor_grid* g) {
   if (g->scratch) cudaFree(g->scratch);
   if (g->dflag) cudaFree(g->dflag);
   if (g->gbar) cudaFree(g->gbar);
+  if (g->rflags) cudaFree(g->rflags);
   if (g->flagbuf) cudaFree(g->flagbuf);
   if (g->djoin) cudaFree(g->djoin);
   if (g->ev0) cudaEventDestroy(g->ev0);
@@ -1230,6 +1231,14 @@ int wave_pass(sor_grid* g, R w, IterCtl ctl) {
 // ------------------------------------------------------------------ K5
 template <typename R>
 int k5_run(sor_grid* g, R w, int solve, int64_t n_iter, double tol, int64_t K, int measure_last) {
+  // register-resident single CTA (K7 form) when the grid fits its window;
+  // SOR_K5_SMEM=1 keeps the shared-memory kernel
+  static int smem_only = -1;
+  if (smem_only < 0) smem_only = getenv("SOR_K5_SMEM") ? 1 : 0;
+  if (!smem_only) {
+    const int rc = launch_resident_single<R>(g, w, solve, n_iter, tol, K, measure_last);
+    if (rc != SOR_E_UNSUPPORTED) return rc;
+  }
   const Slab& s = g->slabs[0];
   const size_t smem = (size_t)(g->rows + 2) * (g->cols + 2) * sizeof(R);
   CU(cudaFuncSetAttribute(k5_small_solve<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1276,7 +1285,9 @@ int end_call(sor_grid* g, DevState* out) {
   return SOR_OK;
 }
 
-int depth_of(const sor_grid* g) { return g->kernel == SOR_KERNEL_TEMPORAL ? g->tdepth : 1; }
+int depth_of(const sor_grid* g) {
+  return (g->kernel == SOR_KERNEL_TEMPORAL || g->kernel == SOR_KERNEL_RESIDENT) ? g->tdepth : 1;
+}
 
 // Max-change mode of T-deep solve passes with check_every == 1: 4 (probe
 // rows, default: 1.09-1.23x the cost of a plain pass on C3 vs 1.10-1.41x for
@@ -1302,6 +1313,13 @@ bool use_persist(const sor_grid* g) {
   const Slab& s = g->slabs[0];
   const double planes = 2.0 * (double)s.nstore * (double)g->pitch * (double)g->esz;
   return planes <= 48.0 * (1 << 20);
+}
+
+// K7 (SOR_KERNEL_RESIDENT, one slab, SOR): register-resident grid, multi-CTA
+// (iterate) or one CTA (iterate and solve) when it fits (resident.cuh).
+bool use_resident(const sor_grid* g, bool single) {
+  if (g->kernel != SOR_KERNEL_RESIDENT || !single_part(g) || g->method != 0) return false;
+  return resident_fits(g, single ? 1 : g->tdepth, single);
 }
 
 template <typename R>
@@ -1345,6 +1363,19 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
       if (c.ck) g->st.checks += 1;
     }
     return SOR_OK;
+  }
+  if (!base.solve && k_from == 1 && use_resident(g, false)) {
+    // K7: the whole iterate call in one launch
+    const int rc = launch_resident_iterate<R>(g, w, k_to, T, check_last);
+    if (rc != SOR_E_UNSUPPORTED) return rc;
+  }
+  if (!base.solve && k_from == 1 && use_resident(g, true)) {
+    const int rc = launch_resident_single<R>(g, w, 0, k_to, 1.0, 1, check_last ? 1 : 0);
+    if (rc == SOR_OK) {
+      g->st.half_sweeps += 2 * k_to;
+      if (check_last) g->st.checks += 1;
+    }
+    if (rc != SOR_E_UNSUPPORTED) return rc;
   }
   const bool every = base.solve && K == 1 && T > 1;
   while (k <= k_to) {
@@ -1525,8 +1556,11 @@ int solve_impl(sor_grid* g, double omega, double tol, int64_t maxit, int64_t K, 
   bool converged = false;
   int64_t done = maxit;
   double maxc = 0.0;
-  if (g->kernel == SOR_KERNEL_SMALL) {
-    TRY(k5_run<R>(g, w, 1, maxit, tol, K, 0));
+  if (g->kernel == SOR_KERNEL_SMALL || use_resident(g, true)) {
+    if (g->kernel == SOR_KERNEL_SMALL)
+      TRY(k5_run<R>(g, w, 1, maxit, tol, K, 0));
+    else
+      TRY(launch_resident_single<R>(g, w, 1, maxit, tol, K, 0));
     TRY(end_call(g, &hs));
     g->st.checks = hs.checks;
     converged = hs.converged != 0;
@@ -1872,7 +1906,8 @@ int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
       g->kernel = kernel;
       g->tdepth = 1;
       break;
-    case SOR_KERNEL_TEMPORAL: {
+    case SOR_KERNEL_TEMPORAL:
+    case SOR_KERNEL_RESIDENT: {
       if (temporal_depth < 1 || temporal_depth > kMaxT)
         return set_error(nullptr, SOR_E_INVAL, "temporal_depth must be in [1,%d], got %d", kMaxT, temporal_depth);
       // the thinnest slab of any rank (sizes differ by at most one row)
@@ -1944,8 +1979,8 @@ struct MethodGuard {  // run one call with the Jacobi method, then restore SOR
   ~MethodGuard() { g->method = 0; }
 };
 int jacobi_usable(sor_grid* g) {
-  if (g->kernel != SOR_KERNEL_FUSED && g->kernel != SOR_KERNEL_TEMPORAL)
-    return set_error(nullptr, SOR_E_UNSUPPORTED, "Jacobi runs on the FUSED / TEMPORAL kernels only");
+  if (g->kernel != SOR_KERNEL_FUSED && g->kernel != SOR_KERNEL_TEMPORAL && g->kernel != SOR_KERNEL_RESIDENT)
+    return set_error(nullptr, SOR_E_UNSUPPORTED, "Jacobi runs on the FUSED / TEMPORAL / RESIDENT kernels only");
   return SOR_OK;
 }
 }  // namespace

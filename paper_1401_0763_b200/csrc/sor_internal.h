@@ -88,6 +88,8 @@ struct sor_grid {
   unsigned int* dflag = nullptr;
   unsigned int* gbar = nullptr;  // K6: grid-barrier counter of the persistent kernel
   bool persist_off = false;      // K6 tiles did not fit in one wave on this handle
+  unsigned long long* rflags = nullptr;  // K7: per-block pass flags (stride 16 words), allocated on first use
+  uint64_t rseq = 0;                     // K7: flag base of the next launch
   int rank = 0, nranks = 1;
   sorh::Transport transport = sorh::Transport::None;
   ncclComm_t comm = nullptr;
@@ -189,5 +191,14 @@ int launch_wave_persist(sor_grid* g, const Slab& s, R w, int npasses, unsigned* 
 template <typename R, int T, int CK, bool LINK>
 int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fused_fin);
 bool use_wave2(const sor_grid* g, int T);
+
+// K7 (resident.cu): the grid register-resident across the SMs.  Iterate
+// passes of T with neighbour-only exchange (multi-CTA), or one CTA running
+// Algorithm 1's loop (single).  SOR_E_UNSUPPORTED if the grid does not fit.
+template <typename R>
+int launch_resident_iterate(sor_grid* g, R w, int64_t iters, int T, bool check_last);
+template <typename R>
+int launch_resident_single(sor_grid* g, R w, int solve, int64_t n_iter, double tol, int64_t K, int check_last);
+bool resident_fits(const sor_grid* g, int T, bool single);
 
 }  // namespace sorh

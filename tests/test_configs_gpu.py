@@ -39,7 +39,7 @@ def test_c1_full(gpu, orc):
     ref = cfg.init()
     rr = orc.solve(ref, cfg.omega, cfg.tol, cfg.maxit, 1)
     assert rr.converged and rr.iters == 1785          # SURVEY P11 (derived), oracle authoritative
-    for kernel, T in (("small", 1), ("temporal", 4)):
+    for kernel, T in (("small", 1), ("temporal", 4), ("resident", 1)):
         with gpu.Grid.create(cfg.init()) as g:
             g.set_kernel(kernel, T)
             r = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1)
@@ -48,7 +48,7 @@ def test_c1_full(gpu, orc):
         assert np.array_equal(out, ref)
 
 
-@pytest.mark.parametrize("kernel,T", [("temporal", 4), ("fused", 1)])
+@pytest.mark.parametrize("kernel,T", [("temporal", 4), ("fused", 1), ("resident", 3), ("resident", 4)])
 def test_c2_full(gpu, orc, kernel, T):
     cfg = SI.config("C2")
     ref = cfg.init()

@@ -14,7 +14,8 @@ import sor_inputs as SI
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4), ("natural", 1)]
+KERNELS = [("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4), ("natural", 1),
+           ("resident", 2), ("resident", 3), ("resident", 4)]
 
 
 @pytest.mark.parametrize("seed", [11, 12])

@@ -17,7 +17,8 @@ import sor_inputs as SI
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [("natural", 1), ("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4)]
+KERNELS = [("natural", 1), ("fused", 1), ("temporal", 2), ("temporal", 3), ("temporal", 4),
+           ("resident", 1), ("resident", 2), ("resident", 3), ("resident", 4)]
 SIZES = [(1, 1), (1, 9), (7, 1), (2, 2), (3, 5), (8, 8), (31, 33), (64, 64), (65, 127),
          (130, 257), (257, 130), (300, 517)]
 
