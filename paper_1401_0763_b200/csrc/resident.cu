@@ -192,8 +192,8 @@ int launch_resident_iterate(sor_grid* g, R w, int64_t iters, int T, bool check_l
   TRY(res_dispatch<R>(g, p, a, true));
   if (trace_path) {
     std::vector<unsigned long long> h(ntr);
+    CU(cudaMemcpyAsync(h.data(), dtrace, ntr * 8, cudaMemcpyDeviceToHost, g->stream));
     CU(cudaStreamSynchronize(g->stream));
-    CU(cudaMemcpy(h.data(), dtrace, ntr * 8, cudaMemcpyDeviceToHost));
     FILE* f = fopen(trace_path, "ab");
     if (f) {
       const int hdr[4] = {p.nbx, p.nby, npasses, T};
