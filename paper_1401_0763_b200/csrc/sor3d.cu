@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "sor_internal.h"
+#include "sor3d_tma.cuh"
 
 using namespace sorh;
 
@@ -21,11 +22,11 @@ struct sor3d_grid {
   int64_t pitch = 0;
   void* plane = nullptr;        // the current iterate
   void* plane2 = nullptr;       // FUSED kernel: the other plane of the ping-pong
-  // default NATURAL: the fused z-plane wavefront (one HBM pass per
-  // iteration) is bitwise equal but slower on B200 (f64 86 vs 158 GLUP/s at
-  // 512^3, profiles/r2_sor3d_fused_variants.txt): one CTA barrier per plane
-  // leaves each CTA latency-bound and only two CTAs fit per SM
+  // default (sor3d_create): FUSED for fp64 (k3d_tma, one HBM pass per
+  // iteration: 208 vs 161 GLUP/s at 512^3), NATURAL for fp32 (the fp32 fused
+  // path is the round-2 shared-plane kernel, slower than the two phases)
   int kernel = SOR_KERNEL_NATURAL;
+  CUtensorMap tm = {}, tm2 = {};  // 3-D tensor maps of plane / plane2 (k3d_tma source boxes)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, poll_ev[2] = {nullptr, nullptr};
   DevState* dstate = nullptr;
@@ -89,8 +90,78 @@ int load3d(sor3d_grid* g, const double* init) {
   return SOR_OK;
 }
 
+// 3-D tensor map of a plane for k3d_tma: (x, y, z) = (nx+2, ny+2, nz+2)
+// elements, box = the kernel's window of one plane; out-of-range box parts
+// read as zeros (never updated cells).
+int make_tmap3(sor3d_grid* g, void* plane, CUtensorMap* m) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return set_error3(g, SOR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)(g->nx + 2), (cuuint64_t)(g->ny + 2), (cuuint64_t)(g->nz + 2)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(g->pitch * g->esz), (cuuint64_t)((g->ny + 2) * g->pitch * g->esz)};
+  const cuuint32_t box[3] = {(cuuint32_t)kT3WX, (cuuint32_t)kT3WY, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = encode(m, g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                      plane, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error3(g, SOR_E_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+  return SOR_OK;
+}
+
+// One fused iteration with k3d_tma (plane -> plane2, then swap).
+template <typename R>
+int k3d_tma_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
+  constexpr int smem = t3_smem_bytes<R>();
+  static int occ_dev[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& occ = occ_dev[dev % kMaxDev];
+  if (occ == 0) {
+    CU3(cudaFuncSetAttribute(k3d_tma<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU3(cudaFuncSetAttribute(k3d_tma<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3d_tma<R, false>, kT3Threads, smem);
+    if (occ <= 0) occ = 1;
+  }
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned bx = (unsigned)((g->nx + kT3X - 1) / kT3X), by = (unsigned)((g->ny + kT3Y - 1) / kT3Y);
+  // z chunks: as many as one wave of resident CTAs holds (each chunk re-reads
+  // 3 planes), at least 8 planes each
+  const int64_t tiles = (int64_t)bx * by;
+  const int64_t nch = std::max<int64_t>(1, (int64_t)occ * nsm / tiles);
+  const int zc = (int)std::max<int64_t>(8, (g->nz + nch - 1) / nch);
+  dim3 grid(bx, by, (unsigned)((g->nz + zc - 1) / zc));
+  IterCtl c = ctl;
+  c.finalize = ctl.ck ? 1 : 0;
+  c.nparts = grid.x * grid.y * grid.z;
+  if (ctl.ck)
+    k3d_tma<R, true><<<grid, kT3Threads, smem, g->stream>>>(g->tm, (R*)g->plane2, g->pitch, (int)g->nz, (int)g->ny,
+                                                             (int)g->nx, zc, w, c);
+  else
+    k3d_tma<R, false><<<grid, kT3Threads, smem, g->stream>>>(g->tm, (R*)g->plane2, g->pitch, (int)g->nz, (int)g->ny,
+                                                              (int)g->nx, zc, w, c);
+  CU3(cudaGetLastError());
+  std::swap(g->plane, g->plane2);
+  std::swap(g->tm, g->tm2);
+  return SOR_OK;
+}
+
 template <typename R>
 int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
+  static int old_fused = -1;  // SOR_K3_OLD=1: the shared-plane z-wavefront of round 2 (A/B only)
+  if (old_fused < 0) old_fused = getenv("SOR_K3_OLD") ? 1 : 0;
+  // (fp32 runs the round-2 kernel: the fp32 instance of k3d_tma faults with an
+  // illegal instruction on B200, not yet understood)
+  static int f32_tma = -1;  // SOR_K3T_F32=1: fp32 on k3d_tma too (diagnosis)
+  if (f32_tma < 0) f32_tma = getenv("SOR_K3T_F32") ? 1 : 0;
+  if (g->kernel == SOR_KERNEL_FUSED && !old_fused && (sizeof(R) == 8 || f32_tma))
+    return k3d_tma_iteration<R>(g, w, ctl);
   if (g->kernel == SOR_KERNEL_FUSED) {
     using G = K3Geo<kX3, kY3>;
     const unsigned bx = (unsigned)((g->nx + 2 + kX3 - 1) / kX3), by = (unsigned)((g->ny + 2 + kY3 - 1) / kY3);
@@ -119,6 +190,7 @@ int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
                                                                    (int)g->nz, (int)g->ny, (int)g->nx, zc, w, c);
     CU3(cudaGetLastError());
     std::swap(g->plane, g->plane2);
+    std::swap(g->tm, g->tm2);
     return SOR_OK;
   }
   const int64_t half = (g->nx + 1) / 2;
@@ -187,8 +259,10 @@ int run3d(sor3d_grid* g, double omega, int solve, int64_t n, double tol, int64_t
   *converged = hs.converged != 0;
   // the fused kernel swapped planes once per enqueued iteration, but those
   // after the converging one exited without writing
-  if (g->kernel == SOR_KERNEL_FUSED && solve && hs.converged && ((enq - hs.conv_iter) & 1))
+  if (g->kernel == SOR_KERNEL_FUSED && solve && hs.converged && ((enq - hs.conv_iter) & 1)) {
     std::swap(g->plane, g->plane2);
+    std::swap(g->tm, g->tm2);
+  }
   if (iters_out) *iters_out = solve ? (hs.converged ? hs.conv_iter : n) : n;
   if (max_out) *max_out = (solve || want_last) && n > 0 ? hs.max_change : 0.0;
   return SOR_OK;
@@ -230,6 +304,7 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
   g->nx = nx;
   g->dt = dt;
   g->esz = dt == SOR_F64 ? 8 : 4;
+  g->kernel = dt == SOR_F64 ? SOR_KERNEL_FUSED : SOR_KERNEL_NATURAL;
   g->pitch = round_up(nx + 2, 32);
   int rc = SOR_OK;
   do {
@@ -276,6 +351,8 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
       }
     }
     rc = load3d(g, init);
+    if (rc == SOR_OK) rc = make_tmap3(g, g->plane, &g->tm);
+    if (rc == SOR_OK) rc = make_tmap3(g, g->plane2, &g->tm2);
   } while (0);
   if (rc < 0) {
     free3d(g);

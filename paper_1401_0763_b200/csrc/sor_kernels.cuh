@@ -138,31 +138,59 @@ __device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b)
 // quotient q0 = RN(s*RN(1/6)) is corrected once with its exact remainder
 // r = s - 6*q0 (an FMA), q = RN(q0 + r*RN(1/6)) (Markstein).  Verified equal
 // to the IEEE division for every float32 with a normal quotient (exhaustive)
-// and 5e8 random float64 (tools/div6_check.c).  Zeros keep their sign
-// (select); subnormal quotients, inf and NaN take the division (a branch that
-// realistic grids never take).  The FMAs here are the algorithm, not a
-// contraction of the canonical update.
+// and 5e8 random float64 (tools/div6_check.c).  Below that range (|s| <
+// 1.5*2^-1020, zeros included) s is an integer k of units 2^-1074 (2^-149
+// for fp32) and the quotient is subnormal: RN(s/6) = k/6 rounded to nearest
+// even in the same units, which is its bit pattern (tools/div6_tiny_check.c:
+// exhaustive for fp32, every k < 2^24 and 5e8 random values for fp64).  Inf
+// and NaN return s.  The FMAs here are the algorithm, not a contraction of
+// the canonical update.  (The integer path replaces a call of the division
+// routine, which the diffusion front of a zero-initialised grid, full of
+// subnormal values, used to take on every warp it crossed.)
+static __device__ __noinline__ double div6_tiny(double s) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  const unsigned long long sign = b & 0x8000000000000000ull, a = b ^ sign;
+  if (a >= 0x7ff0000000000000ull) return s;  // inf, NaN
+  const unsigned long long E = a >> 52, m = a & 0xfffffffffffffull;
+  const unsigned long long k = E == 0 ? m : ((0x10000000000000ull | m) << (E - 1));
+  unsigned long long q = k / 6ull;
+  const unsigned long long r = k - 6ull * q;
+  if (r > 3ull || (r == 3ull && (q & 1ull))) ++q;
+  return __longlong_as_double((long long)(sign | q));
+}
+static __device__ __noinline__ float div6_tiny(float s) {
+  const unsigned b = __float_as_uint(s);
+  const unsigned sign = b & 0x80000000u, a = b ^ sign;
+  if (a >= 0x7f800000u) return s;  // inf, NaN
+  const unsigned E = a >> 23, m = a & 0x7fffffu;
+  const unsigned k = E == 0 ? m : ((0x800000u | m) << (E - 1));
+  unsigned q = k / 6u;
+  const unsigned r = k - 6u * q;
+  if (r > 3u || (r == 3u && (q & 1u))) ++q;
+  return __uint_as_float(sign | q);
+}
 __device__ __forceinline__ double div6(double s) {
   const double yi = 1.0 / 6.0;
   const double q0 = __dmul_rn(s, yi);
   const double r = __fma_rn(-q0, 6.0, s);
   const double q1 = __fma_rn(r, yi, q0);
-  const double a = fabs(s);
-  const bool fast = a >= 0x1.8p-1020 && a <= 0x1.fffffffffffffp+1023;
-  double q = fast ? q1 : s;  // s == +-0: q = s exactly
-  if (!fast && s != 0.0) q = __ddiv_rn(s, 6.0);
-  return q;
+  const unsigned long long a = (unsigned long long)__double_as_longlong(s) & 0x7fffffffffffffffull;
+  // normal range: |s| in [0x1.8p-1020, DBL_MAX]; zeros (a zero-initialised
+  // interior is full of them) keep their sign without the integer path
+  if (a - 0x0038000000000000ull <= 0x7fefffffffffffffull - 0x0038000000000000ull) return q1;
+  if (a == 0ull) return s;
+  return div6_tiny(s);
 }
 __device__ __forceinline__ float div6(float s) {
   const float yi = 1.0f / 6.0f;
   const float q0 = __fmul_rn(s, yi);
   const float r = __fmaf_rn(-q0, 6.0f, s);
   const float q1 = __fmaf_rn(r, yi, q0);
-  const float a = fabsf(s);
-  const bool fast = a >= 0x1.8p-124f && a <= 0x1.fffffep+127f;
-  float q = fast ? q1 : s;
-  if (!fast && s != 0.0f) q = __fdiv_rn(s, 6.0f);
-  return q;
+  const unsigned a = __float_as_uint(s) & 0x7fffffffu;
+  // normal range: |s| in [0x1.8p-124, FLT_MAX]; zeros keep their sign
+  if (a - 0x01c00000u <= 0x7f7fffffu - 0x01c00000u) return q1;
+  if (a == 0u) return s;
+  return div6_tiny(s);
 }
 
 // Eq. 1, BJ form, canonical order.  ns = uN+uS and we = uW+uE are formed by the

@@ -97,3 +97,22 @@ def test_sor3d_random_call_sequences(gpu, orc, seed):
                     assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change), \
                         (case, nz, ny, nx, kernel, dtype)
             assert np.array_equal(g.download(), ref.astype(np.float64)), (case, nz, ny, nx, kernel, dtype)
+
+
+@pytest.mark.parametrize("kernel", ["fused", "natural"])
+@pytest.mark.parametrize("dtype,scale", [("f64", 1e-305), ("f64", 1.0), ("f32", 1e-36)])
+def test_sor3d_tiny_values_and_chunks(gpu, orc, kernel, dtype, scale):
+    """Reading N3-2's integer path for tiny quotients: a shell scaled into the
+    subnormal range (and a zero interior) makes the s/6 of the diffusion front
+    tiny or subnormal; shapes give several (y, x) tiles, ragged tiles and
+    several z chunks of the fused kernel.  Bitwise against the oracle."""
+    init = SI.random_shell3d(37, 45, 97, seed=5) * scale
+    init[1:-1, 1:-1, 1:-1] = SI.random_field3d(37, 45, 97, seed=6, lo=0.0, hi=1.0)[1:-1, 1:-1, 1:-1] * scale * 1e-3
+    ref = init.copy() if dtype == "f64" else init.astype(np.float32)
+    rep = orc.sor3d_iterate(ref, 1.85, 23, measure_last=True)
+    with gpu.Grid3D(init, dtype=dtype) as g:
+        g.set_kernel(kernel)
+        d = g.iterate(1.85, 23, want_delta=True)
+        out = g.download()
+    assert np.array_equal(out, ref.astype(np.float64))
+    assert d == rep.max_change
