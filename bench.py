@@ -270,12 +270,15 @@ def run_next(args):
         init_h = SI.random_shell3d(n, n, n, seed=7)
         iters, units = 50, n ** 3
         g = P.Grid3D(init_h)
+        k3 = "natural" if args.kernel == "natural" else "fused"
+        g.set_kernel(k3)
         run = lambda k: g.iterate(1.9, k)                  # noqa: E731
         reset_d = None
-        bytes_per_update = 32.0
-        kname, workload = "k3d_half_sweep<f64> (red + black)", f"3-D red-black SOR (NEXT-3): 512^3 f64, omega 1.9, {iters} iterations"
+        bytes_per_update = 32.0 if k3 == "natural" else 16.0
+        kname = "k3d_half_sweep<f64> (red + black)" if k3 == "natural" else "k3d_tma<f64> (one pass)"
+        workload = f"3-D red-black SOR (NEXT-3): 512^3 f64, omega 1.9, {iters} iterations, {k3} kernel"
         elapsed = lambda: g.elapsed_ms                     # noqa: E731
-        launches = lambda: 2 * iters                       # noqa: E731
+        launches = lambda: (2 if k3 == "natural" else 1) * iters  # noqa: E731
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     for _ in range(args.warmup):
         run(iters)
@@ -317,6 +320,7 @@ def run_next(args):
             g.download(hout)
         else:
             g3 = P.Grid3D(hin.numpy())
+            g3.set_kernel(k3)
             g3.iterate(1.9, iters)
             g3.download(hout.numpy())
             g3.close()
@@ -424,6 +428,36 @@ def measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, p
 
 
 # ------------------------------------------------------------------ our arm
+def measure_small(P, torch):
+    """BJ configs[0] and configs[1] (the latency configs) on one GPU with the
+    register-resident K7 kernel (SOR_KERNEL_RESIDENT): C1 solved on one CTA
+    with the stop test on the device, C2 iterated on one block per SM with
+    T = 3 passes; device time of the call (CUDA events), best of 5, grid
+    reset from HBM before each run.  The per-iteration time is the figure of
+    merit (both grids are L2/register resident; there is no HBM roofline)."""
+    out = {}
+    for name, T in (("C1", 1), ("C2", 3)):
+        cfg = SI.config(name)
+        dinit = torch.from_numpy(cfg.init()).cuda()
+        with P.Grid.create(dinit) as g:
+            g.set_kernel("resident", T)
+            best, iters = 1e30, 0
+            for rep in range(6):
+                g.reset(dinit)
+                if name == "C1":
+                    iters = g.solve(cfg.omega, cfg.tol, cfg.maxit, 1).iters
+                else:
+                    g.iterate(cfg.omega, cfg.iters)
+                    iters = cfg.iters
+                if rep:
+                    best = min(best, g.elapsed_ms)
+            launches = g.stats["kernel_launches"]
+        out[name] = {"us_per_iteration": best * 1e3 / iters, "iterations": iters, "ms": best,
+                     "glups": cfg.rows * cfg.cols * iters / (best * 1e-3) / 1e9, "kernel_launches": launches,
+                     "kernel": "resident (K7)", "temporal_depth": T}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -443,6 +477,7 @@ def main():
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1: halo/max transport (ipc: device-initiated pushes over CUDA IPC)")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (32768^2) sub-record")
+    ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 (latency configs) sub-record")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--method", default="sor", choices=["sor", "jacobi", "sor3d"],
                     help="sor: the headline path; jacobi / sor3d: the NEXT-2 / NEXT-3 rows (1 GPU)")
@@ -662,6 +697,8 @@ def main():
     # 32768x32768 f64, omega_opt, 200 iterations, temporally blocked T=4)
     if not args.no_c5 and args.config == "C3":
         line["c5"] = measure_c5(P, torch, dist, make_grid, transport, world, rank, local, args, pk, pk_kind)
+    if rank == 0 and world == 1 and args.config == "C3" and not args.no_small:
+        line["small_configs"] = measure_small(P, torch)
     if rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_window)
     if rank == 0:
