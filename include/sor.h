@@ -183,9 +183,9 @@ int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every
  * (correctly rounded), u' = u + omega*(a - u) (reading N3-1).
  * iterate / solve / download / errors as the 2-D calls, exact maxima.
  * Kernels (sor3d_set_kernel): SOR_KERNEL_NATURAL (two in-place colour
- * phases; the fp32 default) or SOR_KERNEL_FUSED (the fp64 default: one HBM
- * pass per iteration, a z-plane wavefront over TMA-staged planes, src ->
- * dst, two planes per CTA barrier); bitwise equal.                          */
+ * phases) or SOR_KERNEL_FUSED (the default: one HBM pass per iteration, a
+ * z-plane wavefront over TMA-staged planes, src -> dst, two planes per CTA
+ * barrier); bitwise equal.                                                  */
 typedef struct sor3d_grid sor3d_grid;
 int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const double* init, sor_dtype dt);
 int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_change);

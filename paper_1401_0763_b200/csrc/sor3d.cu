@@ -22,9 +22,8 @@ struct sor3d_grid {
   int64_t pitch = 0;
   void* plane = nullptr;        // the current iterate
   void* plane2 = nullptr;       // FUSED kernel: the other plane of the ping-pong
-  // default (sor3d_create): FUSED for fp64 (k3d_tma, one HBM pass per
-  // iteration: 208 vs 161 GLUP/s at 512^3), NATURAL for fp32 (the fp32 fused
-  // path is the round-2 shared-plane kernel, slower than the two phases)
+  // default (sor3d_create): FUSED (k3d_tma, one HBM pass per iteration: 208
+  // vs 161 GLUP/s in fp64 and 330 vs 225 in fp32 at 512^3)
   int kernel = SOR_KERNEL_NATURAL;
   CUtensorMap tm = {}, tm2 = {};  // 3-D tensor maps of plane / plane2 (k3d_tma source boxes)
   cudaStream_t stream = nullptr;
@@ -105,7 +104,8 @@ int make_tmap3(sor3d_grid* g, void* plane, CUtensorMap* m) {
   }
   const cuuint64_t dims[3] = {(cuuint64_t)(g->nx + 2), (cuuint64_t)(g->ny + 2), (cuuint64_t)(g->nz + 2)};
   const cuuint64_t strides[2] = {(cuuint64_t)(g->pitch * g->esz), (cuuint64_t)((g->ny + 2) * g->pitch * g->esz)};
-  const cuuint32_t box[3] = {(cuuint32_t)kT3WX, (cuuint32_t)kT3WY, 1u};
+  const cuuint32_t box[3] = {(cuuint32_t)(g->dt == SOR_F64 ? t3_wxb<double>() : t3_wxb<float>()), (cuuint32_t)kT3WY,
+                             1u};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = encode(m, g->dt == SOR_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                       plane, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -156,12 +156,7 @@ template <typename R>
 int k3d_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
   static int old_fused = -1;  // SOR_K3_OLD=1: the shared-plane z-wavefront of round 2 (A/B only)
   if (old_fused < 0) old_fused = getenv("SOR_K3_OLD") ? 1 : 0;
-  // (fp32 runs the round-2 kernel: the fp32 instance of k3d_tma faults with an
-  // illegal instruction on B200, not yet understood)
-  static int f32_tma = -1;  // SOR_K3T_F32=1: fp32 on k3d_tma too (diagnosis)
-  if (f32_tma < 0) f32_tma = getenv("SOR_K3T_F32") ? 1 : 0;
-  if (g->kernel == SOR_KERNEL_FUSED && !old_fused && (sizeof(R) == 8 || f32_tma))
-    return k3d_tma_iteration<R>(g, w, ctl);
+  if (g->kernel == SOR_KERNEL_FUSED && !old_fused) return k3d_tma_iteration<R>(g, w, ctl);
   if (g->kernel == SOR_KERNEL_FUSED) {
     using G = K3Geo<kX3, kY3>;
     const unsigned bx = (unsigned)((g->nx + 2 + kX3 - 1) / kX3), by = (unsigned)((g->ny + 2 + kY3 - 1) / kY3);
@@ -304,7 +299,7 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
   g->nx = nx;
   g->dt = dt;
   g->esz = dt == SOR_F64 ? 8 : 4;
-  g->kernel = dt == SOR_F64 ? SOR_KERNEL_FUSED : SOR_KERNEL_NATURAL;
+  g->kernel = SOR_KERNEL_FUSED;
   g->pitch = round_up(nx + 2, 32);
   int rc = SOR_OK;
   do {

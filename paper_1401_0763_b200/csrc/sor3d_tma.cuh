@@ -39,6 +39,15 @@ namespace sorb {
 
 constexpr int kT3X = 30, kT3Y = 14;           // tile (x, y)
 constexpr int kT3WX = kT3X + 6, kT3WY = kT3Y + 4;  // window: columns [x0-3, x0+33), rows [y0-2, y0+16)
+// The TMA box starts on a 16-B boundary (a 3-D box whose first column is not
+// 16-B aligned faults with an illegal instruction on B200: fp32 windows
+// starting at x0-3 did): the box starts up to 16/size-2 elements left of
+// x0-3 and is that much wider, rounded to 16 B.
+template <typename R>
+__host__ __device__ constexpr int t3_wxb() {
+  return (kT3WX + (16 / (int)sizeof(R) - 2) + (16 / (int)sizeof(R)) - 1) / (16 / (int)sizeof(R)) *
+         (16 / (int)sizeof(R));
+}
 constexpr int kT3NP = 8;                       // shared plane slots
 constexpr int kT3Pairs = (kT3X + 2) / 2;       // column pairs of the ring-1 region (16: a half warp)
 constexpr int kT3Threads = kT3Pairs * (kT3Y + 2);  // 256: 8 warps, each two ring-1 rows of one parity
@@ -47,7 +56,7 @@ constexpr int kT3Threads = kT3Pairs * (kT3Y + 2);  // 256: 8 warps, each two rin
 // are 128-B aligned)
 template <typename R>
 __host__ __device__ constexpr int t3_slot_elems() {
-  return (kT3WX * kT3WY * (int)sizeof(R) + 127) / 128 * 128 / (int)sizeof(R);
+  return (t3_wxb<R>() * kT3WY * (int)sizeof(R) + 127) / 128 * 128 / (int)sizeof(R);
 }
 template <typename R>
 __host__ __device__ constexpr int t3_smem_bytes() {
@@ -130,7 +139,7 @@ struct T3Thread {
 template <typename R, bool CHECK, int E>
 __device__ __forceinline__ R t3_red(const T3Thread<R>& t, bool red_z, bool red_own, R w, const R* sm, R* s0,
                                     const R* sp, unsigned long long& dmax) {
-  constexpr int WX = kT3WX;
+  constexpr int WX = t3_wxb<R>();
   R n0, n1, c0, c1, s0v, s1v, u0, u1, d0, d1;
   Pair2<R>::ld(s0 + t.off - WX, n0, n1);
   Pair2<R>::ld(s0 + t.off, c0, c1);
@@ -155,7 +164,7 @@ __device__ __forceinline__ R t3_red(const T3Thread<R>& t, bool red_z, bool red_o
 template <typename R, bool CHECK, int E>
 __device__ __forceinline__ void t3_black(const T3Thread<R>& t, R w, const R* sb, R rU, R rD, R* out,
                                          unsigned long long& dmax) {
-  constexpr int WX = kT3WX;
+  constexpr int WX = t3_wxb<R>();
   R n0, n1, c0, c1, s0v, s1v;
   Pair2<R>::ld(sb + t.off - WX, n0, n1);
   Pair2<R>::ld(sb + t.off, c0, c1);
@@ -192,7 +201,9 @@ __global__ void __launch_bounds__(kT3Threads, 5)
   const int wr = 1 + ty, wc = 2 + 2 * p;        // window row / first column of the pair
   const int y = y0 - 2 + wr, xa = x0 - 3 + wc;  // global row / first column
   T3Thread<R> t;
-  t.off = wr * kT3WX + wc;
+  // box origin: x0-3 rounded down to 16 B; the window starts xd columns into it
+  const int xs = (x0 - 3) & ~(16 / (int)sizeof(R) - 1), xd = (x0 - 3) - xs;
+  t.off = wr * t3_wxb<R>() + wc + xd;
   t.trow = wr >= 2 && wr < 2 + kT3Y;
   const bool yin = y >= 1 && y <= ny;
   const bool tcol0 = wc >= 3 && wc < 3 + kT3X, tcol1 = wc + 1 >= 3 && wc + 1 < 3 + kT3X;
@@ -218,11 +229,11 @@ __global__ void __launch_bounds__(kT3Threads, 5)
     mbar_fence_init();
   }
   __syncthreads();
-  constexpr uint32_t kBytes = (uint32_t)(kT3WX * kT3WY * sizeof(R));  // one box
+  constexpr uint32_t kBytes = (uint32_t)(t3_wxb<R>() * kT3WY * sizeof(R));  // one box
   auto issue = [&](int q) {  // plane z0-2+q into its slot
     const uint32_t b = bar0 + 8u * (q % kT3NP);
     mbar_expect_tx(b, kBytes);
-    tma_box3(smem_u32(slot + (q % kT3NP) * SP), &tm, x0 - 3, y0 - 2, z0 - 2 + q, b);
+    tma_box3(smem_u32(slot + (q % kT3NP) * SP), &tm, xs, y0 - 2, z0 - 2 + q, b);
   };
   if (tid == 0)  // planes 0..4; interval q issues q+4, q+5
     for (int q = 0; q < min(5, nq); ++q) issue(q);
