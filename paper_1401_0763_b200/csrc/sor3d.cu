@@ -131,11 +131,23 @@ int k3d_tma_iteration(sor3d_grid* g, R w, const IterCtl& ctl) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const unsigned bx = (unsigned)((g->nx + kT3X - 1) / kT3X), by = (unsigned)((g->ny + kT3Y - 1) / kT3Y);
-  // z chunks: as many as one wave of resident CTAs holds (each chunk re-reads
-  // 3 planes), at least 8 planes each
-  const int64_t tiles = (int64_t)bx * by;
-  const int64_t nch = std::max<int64_t>(1, (int64_t)occ * nsm / tiles);
-  const int zc = (int)std::max<int64_t>(8, (g->nz + nch - 1) / nch);
+  // z chunks: minimise waves x planes per CTA (a chunk also reads ~5 planes
+  // of warm-up), so the last wave is not a short tail of CTAs (e.g. 512^3
+  // fp64: 666 tiles on 592 resident CTAs -> 8 chunks of 64 planes, 9 full
+  // waves), chunks of at least 8 planes
+  const int64_t tiles = (int64_t)bx * by, slots = (int64_t)occ * nsm;
+  int64_t best_cost = -1, nch = 1;
+  for (int64_t c = 1; c <= 64; ++c) {
+    const int64_t zc_c = (g->nz + c - 1) / c;
+    if (c > 1 && zc_c < 8) break;
+    const int64_t waves = (tiles * ((g->nz + zc_c - 1) / zc_c) + slots - 1) / slots;
+    const int64_t cost = waves * (zc_c + 5);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      nch = c;
+    }
+  }
+  const int zc = (int)((g->nz + nch - 1) / nch);
   dim3 grid(bx, by, (unsigned)((g->nz + zc - 1) / zc));
   IterCtl c = ctl;
   c.finalize = ctl.ck ? 1 : 0;

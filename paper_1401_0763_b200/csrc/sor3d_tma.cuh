@@ -133,58 +133,50 @@ struct T3Thread {
   bool st2, st0, st1;  // store of the finished pair: both cells as one 16-B vector, cell 0, cell 1
 };
 
-// red(z) at the pair's column E, in place into slot s0 (U from sm, D from
-// sp); returns the cell's value after the red phase (its old value if it is
-// not updated).
-template <typename R, bool CHECK, int E>
-__device__ __forceinline__ R t3_red(const T3Thread<R>& t, bool red_z, bool red_own, R w, const R* sm, R* s0,
-                                    const R* sp, unsigned long long& dmax) {
-  constexpr int WX = t3_wxb<R>();
-  R n0, n1, c0, c1, s0v, s1v, u0, u1, d0, d1;
-  Pair2<R>::ld(s0 + t.off - WX, n0, n1);
-  Pair2<R>::ld(s0 + t.off, c0, c1);
-  Pair2<R>::ld(s0 + t.off + WX, s0v, s1v);
-  Pair2<R>::ld(sm + t.off, u0, u1);
-  Pair2<R>::ld(sp + t.off, d0, d1);
-  const R outside = s0[t.off + (E == 0 ? -1 : 2)];
-  const R uN = E ? n1 : n0, uS = E ? s1v : s0v, u = E ? c1 : c0;
-  const R uW = E ? c0 : outside, uE = E ? outside : c1;
-  const R uU = E ? u1 : u0, uD = E ? d1 : d0;
-  const R s = radd(radd(radd(uN, uS), radd(uW, uE)), radd(uU, uD));
-  const R v = radd(u, rmul(w, rsub(div6_v(s), u)));
-  const bool upd = red_z && t.upd[E];
-  if (upd) s0[t.off + E] = v;
-  if (CHECK && upd && red_own && t.trow && t.chk[E]) dmax = umax64(dmax, delta_bits(v, u));
-  return upd ? v : u;
+// A row pair of a slot: cells 0, 1 of the thread's pair in window row wr+dr.
+template <typename R>
+struct T3Row {
+  R a, b;
+  __device__ __forceinline__ R at(int e) const { return e ? b : a; }
+};
+template <typename R>
+__device__ __forceinline__ T3Row<R> t3_row(const R* sl, int off) {
+  T3Row<R> r;
+  Pair2<R>::ld(sl + off, r.a, r.b);
+  return r;
 }
 
-// black(zb) at the pair's column E over the tile, from slot sb (the new reds
-// of plane zb, its own old value), vertical reds rU (zb-1) and rD (zb+1) of
-// the same column; the finished pair of plane zb goes to out.
+// Eq. 1 in 3-D for the pair's cell E of a plane: in-plane rows N (above), C
+// (own row), S (below), the neighbour outside the pair, vertical U, D.
+template <typename R, int E>
+__device__ __forceinline__ R t3_update(const T3Row<R>& N, const T3Row<R>& C, const T3Row<R>& S, R outside, R uU,
+                                       R uD, R w) {
+  const R uW = E ? C.a : outside, uE = E ? outside : C.b;
+  const R s = radd(radd(radd(N.at(E), S.at(E)), radd(uW, uE)), radd(uU, uD));
+  const R u = C.at(E);
+  return radd(u, rmul(w, rsub(div6_v(s), u)));
+}
+
+// black(zb) at column E over the tile from slot rows N, C, S (its new reds
+// and its own old value) and vertical reds rU (zb-1), rD (zb+1) of the same
+// column; the finished pair of plane zb goes to out.
 template <typename R, bool CHECK, int E>
-__device__ __forceinline__ void t3_black(const T3Thread<R>& t, R w, const R* sb, R rU, R rD, R* out,
+__device__ __forceinline__ void t3_black(const T3Thread<R>& t, R w, const T3Row<R>& N, const T3Row<R>& C,
+                                         const T3Row<R>& S, R outside, R rU, R rD, R* out,
                                          unsigned long long& dmax) {
-  constexpr int WX = t3_wxb<R>();
-  R n0, n1, c0, c1, s0v, s1v;
-  Pair2<R>::ld(sb + t.off - WX, n0, n1);
-  Pair2<R>::ld(sb + t.off, c0, c1);
-  Pair2<R>::ld(sb + t.off + WX, s0v, s1v);
-  const R outside = sb[t.off + (E == 0 ? -1 : 2)];
-  const R uN = E ? n1 : n0, uS = E ? s1v : s0v, u = E ? c1 : c0;
-  const R uW = E ? c0 : outside, uE = E ? outside : c1;
-  const R s = radd(radd(radd(uN, uS), radd(uW, uE)), radd(rU, rD));
-  const R v = radd(u, rmul(w, rsub(div6_v(s), u)));
+  const R v = t3_update<R, E>(N, C, S, outside, rU, rD, w);
+  const R u = C.at(E);
   const R b = t.upd[E] ? v : u;
   if (CHECK && t.upd[E] && t.chk[E]) dmax = umax64(dmax, delta_bits(v, u));
   // the finished pair: black b at E, red (slot) at 1-E
-  const R o0 = E ? c0 : b, o1 = E ? b : c1;
+  const R o0 = E ? C.a : b, o1 = E ? b : C.b;
   if (t.st2) Pair2<R>::st(out, o0, o1);
   if (t.st0) out[0] = o0;
   if (t.st1) out[1] = o1;
 }
 
 template <typename R, bool CHECK>
-__global__ void __launch_bounds__(kT3Threads, 5)
+__global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
     k3d_tma(const __grid_constant__ CUtensorMap tm, R* __restrict__ dst, long long pitch, int nz, int ny, int nx,
             int zc, R w, IterCtl ctl) {
   extern __shared__ __align__(128) unsigned char t3_smem[];
@@ -235,8 +227,8 @@ __global__ void __launch_bounds__(kT3Threads, 5)
     mbar_expect_tx(b, kBytes);
     tma_box3(smem_u32(slot + (q % kT3NP) * SP), &tm, xs, y0 - 2, z0 - 2 + q, b);
   };
-  if (tid == 0)  // planes 0..4; interval q issues q+4, q+5
-    for (int q = 0; q < min(5, nq); ++q) issue(q);
+  if (tid == 0)  // planes 0..NP-4; interval q issues q+NP-4, q+NP-3 (into the slots of q-4, q-3)
+    for (int q = 0; q < min(kT3NP - 3, nq); ++q) issue(q);
   // the thread's reds (value after the red phase) of planes z-3, z-2, z-1
   R r3 = R(0), r2 = R(0), r1 = R(0);
   unsigned long long dmax = 0ull;
@@ -252,8 +244,8 @@ __global__ void __launch_bounds__(kT3Threads, 5)
     __syncthreads();  // earlier reds are written; slots of planes z-4, z-3 are free
     if (tid == 0) {
       fence_proxy_async_smem();  // slots being refilled were written by the generic proxy
-      if (q + 4 < nq) issue(q + 4);
-      if (q + 5 < nq) issue(q + 5);
+      if (q + kT3NP - 4 < nq) issue(q + kT3NP - 4);
+      if (q + kT3NP - 3 < nq) issue(q + kT3NP - 3);
     }
     // planes z+1, z+2 (z-2 .. z arrived for earlier intervals or the first)
     mbar_wait(bar0 + 8u * ((q + 1) % kT3NP), (uint32_t)(((q + 1) / kT3NP) & 1));
@@ -262,18 +254,57 @@ __global__ void __launch_bounds__(kT3Threads, 5)
       mbar_wait(bar0 + 8u * 0, 0u);
       mbar_wait(bar0 + 8u * 1, 0u);
     }
+    constexpr int WX = t3_wxb<R>();
     R* sl[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) sl[k] = slot + ((q - 2 + k + kT3NP) % kT3NP) * SP;  // planes z-2 .. z+2
-    const R rz = t3_red<R, CHECK, E>(t, (unsigned)(z - zr_lo) <= (unsigned)(zr_hi - zr_lo), z >= z0 && z < z1, w,
-                                     sl[1], sl[2], sl[3], dmax);
-    const R rz1 = t3_red<R, CHECK, E ^ 1>(t, (unsigned)(z + 1 - zr_lo) <= (unsigned)(zr_hi - zr_lo),
-                                          z + 1 >= z0 && z + 1 < z1, w, sl[2], sl[3], sl[4], dmax);
+    // Rows are loaded once per interval and shared between the phases that
+    // read them: slot z-1's own row is red(z)'s U and black(z-1)'s centre,
+    // slot z's own row is red(z)'s centre and red(z+1)'s U (column E^1, which
+    // red(z) does not write), slot z+1's own row is red(z)'s D and red(z+1)'s
+    // centre (read before red(z+1) writes its column).
+    const int o = t.off;
+    const T3Row<R> Bc = t3_row(sl[1], o);
+    const T3Row<R> Cn = t3_row(sl[2], o - WX), Cc = t3_row(sl[2], o), Cs = t3_row(sl[2], o + WX);
+    const T3Row<R> Dn = t3_row(sl[3], o - WX), Dc = t3_row(sl[3], o), Ds = t3_row(sl[3], o + WX);
+    const R Co = sl[2][o + (E == 0 ? -1 : 2)];
+    const R Do = sl[3][o + (E == 0 ? 2 : -1)];
+    const R Fc = sl[4][o + (E ^ 1)];
+    // red(z): column E
+    R rz = Cc.at(E);
+    {
+      const R v = t3_update<R, E>(Cn, Cc, Cs, Co, Bc.at(E), Dc.at(E), w);
+      const bool upd = (unsigned)(z - zr_lo) <= (unsigned)(zr_hi - zr_lo) && t.upd[E];
+      if (upd) {
+        sl[2][o + E] = v;
+        if (CHECK && z >= z0 && z < z1 && t.trow && t.chk[E]) dmax = umax64(dmax, delta_bits(v, rz));
+        rz = v;
+      }
+    }
+    // red(z+1): column E^1
+    R rz1 = Dc.at(E ^ 1);
+    {
+      const R v = t3_update<R, E ^ 1>(Dn, Dc, Ds, Do, Cc.at(E ^ 1), Fc, w);
+      const bool upd = (unsigned)(z + 1 - zr_lo) <= (unsigned)(zr_hi - zr_lo) && t.upd[E ^ 1];
+      if (upd) {
+        sl[3][o + (E ^ 1)] = v;
+        if (CHECK && z + 1 >= z0 && z + 1 < z1 && t.trow && t.chk[E ^ 1]) dmax = umax64(dmax, delta_bits(v, rz1));
+        rz1 = v;
+      }
+    }
     if (t.trow) {
       // black(z-2): column E^1 (red column of plane z-1), reds z-3, z-1
-      if (z - 2 >= z0 && z - 2 < z1) t3_black<R, CHECK, E ^ 1>(t, w, sl[0], r3, r1, out, dmax);
+      if (z - 2 >= z0 && z - 2 < z1) {
+        const T3Row<R> An = t3_row(sl[0], o - WX), Ac = t3_row(sl[0], o), As = t3_row(sl[0], o + WX);
+        const R Ao = sl[0][o + (E == 0 ? 2 : -1)];
+        t3_black<R, CHECK, E ^ 1>(t, w, An, Ac, As, Ao, r3, r1, out, dmax);
+      }
       // black(z-1): column E, reds z-2, z
-      if (z - 1 >= z0 && z - 1 < z1) t3_black<R, CHECK, E>(t, w, sl[1], r2, rz, out + zstride, dmax);
+      if (z - 1 >= z0 && z - 1 < z1) {
+        const T3Row<R> Bn = t3_row(sl[1], o - WX), Bs = t3_row(sl[1], o + WX);
+        const R Bo = sl[1][o + (E == 0 ? -1 : 2)];
+        t3_black<R, CHECK, E>(t, w, Bn, Bc, Bs, Bo, r2, rz, out + zstride, dmax);
+      }
     }
     out += 2 * zstride;
     r3 = r1;
