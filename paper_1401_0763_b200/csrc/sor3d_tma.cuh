@@ -37,8 +37,8 @@
 
 namespace sorb {
 
-constexpr int kT3X = 62, kT3Y = 14;           // tile (x, y)
-constexpr int kT3WX = kT3X + 6, kT3WY = kT3Y + 4;  // window: columns [x0-3, x0+KX+3), rows [y0-2, y0+KY+2)
+constexpr int kT3X = 30, kT3Y = 14;           // tile (x, y)
+constexpr int kT3WX = kT3X + 6, kT3WY = kT3Y + 4;  // window: columns [x0-3, x0+33), rows [y0-2, y0+16)
 // The TMA box starts on a 16-B boundary (a 3-D box whose first column is not
 // 16-B aligned faults with an illegal instruction on B200: fp32 windows
 // starting at x0-3 did): the box starts up to 16/size-2 elements left of
@@ -49,8 +49,8 @@ __host__ __device__ constexpr int t3_wxb() {
          (16 / (int)sizeof(R));
 }
 constexpr int kT3NP = 8;                       // shared plane slots
-constexpr int kT3Pairs = (kT3X + 2) / 2;       // column pairs of the ring-1 region (32: a warp)
-constexpr int kT3Threads = kT3Pairs * (kT3Y + 2);  // 512: 16 warps, one ring-1 row each
+constexpr int kT3Pairs = (kT3X + 2) / 2;       // column pairs of the ring-1 region (16: a half warp)
+constexpr int kT3Threads = kT3Pairs * (kT3Y + 2);  // 256: 8 warps, each two ring-1 rows of one parity
 
 // elements per shared slot: one box, rounded up to 128 B (TMA destinations
 // are 128-B aligned)
@@ -176,7 +176,7 @@ __device__ __forceinline__ void t3_black(const T3Thread<R>& t, R w, const T3Row<
 }
 
 template <typename R, bool CHECK>
-__global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 2 : 2)
+__global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
     k3d_tma(const __grid_constant__ CUtensorMap tm, R* __restrict__ dst, long long pitch, int nz, int ny, int nx,
             int zc, R w, IterCtl ctl) {
   extern __shared__ __align__(128) unsigned char t3_smem[];
@@ -185,8 +185,9 @@ __global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 2 : 2)
   R* slot = reinterpret_cast<R*>(t3_smem);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(t3_smem + kT3NP * SP * sizeof(R));
   const int tid = threadIdx.x;
-  // warp w holds ring-1 row w (one parity per warp)
-  const int p = tid & 31, ty = tid >> 5;
+  const int warp = tid >> 5, half = (tid >> 4) & 1, p = tid & 15;
+  // ring-1 row of the thread: warp w holds rows base, base + 2 (one parity)
+  const int ty = (warp >> 1) * 4 + (warp & 1) + 2 * half;
   const int x0 = 1 + (int)blockIdx.x * kT3X, y0 = 1 + (int)blockIdx.y * kT3Y;
   const int z0 = 1 + (int)blockIdx.z * zc, z1 = min(nz + 1, z0 + zc);  // owned planes [z0, z1)
   const int wr = 1 + ty, wc = 2 + 2 * p;        // window row / first column of the pair
