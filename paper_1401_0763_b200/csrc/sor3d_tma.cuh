@@ -50,7 +50,7 @@ __host__ __device__ constexpr int t3_wxb() {
 }
 constexpr int kT3NP = 8;                       // shared plane slots
 constexpr int kT3Pairs = (kT3X + 2) / 2;       // column pairs of the ring-1 region (16: a half warp)
-constexpr int kT3Threads = kT3Pairs * (kT3Y + 2);  // 256: 8 warps, each two ring-1 rows of one parity
+constexpr int kT3Threads = kT3Pairs * (kT3Y + 2) / 2;  // 128: each thread two adjacent ring-1 rows
 
 // elements per shared slot: one box, rounded up to 128 B (TMA destinations
 // are 128-B aligned)
@@ -123,14 +123,15 @@ __device__ __forceinline__ float div6_v(float s) {
   return q;
 }
 
-// Per-thread constants of k3d_tma (all loop-invariant predicates precomputed).
+// Per-thread constants of k3d_tma (all loop-invariant predicates precomputed):
+// the thread owns the same column pair in two adjacent window rows a, b.
 template <typename R>
 struct T3Thread {
-  int off;        // window offset of the pair: wr * WX + wc
-  bool trow;      // a tile row (black phase)
-  bool upd[2];    // cell e of the pair is interior (in-plane)
-  bool chk[2];    // ... and in a tile column (max-change)
-  bool st2, st0, st1;  // store of the finished pair: both cells as one 16-B vector, cell 0, cell 1
+  int off;          // window offset of the pair in row a: wr_a * WX + wc (row b: + WX)
+  bool trow[2];     // row a / b is a tile row (black phase)
+  bool upd[2][2];   // [row][cell] interior (in-plane)
+  bool chk[2];      // cell in a tile column (max-change)
+  bool st2[2], st0[2], st1[2];  // [row] store of the finished pair: 16-B vector, cell 0, cell 1
 };
 
 // A row pair of a slot: cells 0, 1 of the thread's pair in window row wr+dr.
@@ -157,26 +158,40 @@ __device__ __forceinline__ R t3_update(const T3Row<R>& N, const T3Row<R>& C, con
   return radd(u, rmul(w, rsub(div6_v(s), u)));
 }
 
-// black(zb) at column E over the tile from slot rows N, C, S (its new reds
-// and its own old value) and vertical reds rU (zb-1), rD (zb+1) of the same
-// column; the finished pair of plane zb goes to out.
+// black(zb) of row `r` at column E over the tile from slot rows N, C, S (its
+// new reds and its own old value) and vertical reds rU (zb-1), rD (zb+1) of
+// the same column; the finished pair of plane zb goes to out (tile rows only).
 template <typename R, bool CHECK, int E>
-__device__ __forceinline__ void t3_black(const T3Thread<R>& t, R w, const T3Row<R>& N, const T3Row<R>& C,
+__device__ __forceinline__ void t3_black(const T3Thread<R>& t, int r, R w, const T3Row<R>& N, const T3Row<R>& C,
                                          const T3Row<R>& S, R outside, R rU, R rD, R* out,
                                          unsigned long long& dmax) {
   const R v = t3_update<R, E>(N, C, S, outside, rU, rD, w);
   const R u = C.at(E);
-  const R b = t.upd[E] ? v : u;
-  if (CHECK && t.upd[E] && t.chk[E]) dmax = umax64(dmax, delta_bits(v, u));
+  const bool upd = t.upd[r][E];
+  const R b = upd ? v : u;
+  if (CHECK && upd && t.trow[r] && t.chk[E]) dmax = umax64(dmax, delta_bits(v, u));
   // the finished pair: black b at E, red (slot) at 1-E
   const R o0 = E ? C.a : b, o1 = E ? b : C.b;
-  if (t.st2) Pair2<R>::st(out, o0, o1);
-  if (t.st0) out[0] = o0;
-  if (t.st1) out[1] = o1;
+  if (t.st2[r]) Pair2<R>::st(out, o0, o1);
+  if (t.st0[r]) out[0] = o0;
+  if (t.st1[r]) out[1] = o1;
+}
+
+// red(z) of row `r` at column E, in place into slot sl at offset o.
+template <typename R, bool CHECK, int E>
+__device__ __forceinline__ R t3_red(const T3Thread<R>& t, int r, bool red_z, bool red_own, R w, R* sl, int o,
+                                    const T3Row<R>& N, const T3Row<R>& C, const T3Row<R>& S, R outside, R uU,
+                                    R uD, unsigned long long& dmax) {
+  const R u = C.at(E);
+  const R v = t3_update<R, E>(N, C, S, outside, uU, uD, w);
+  const bool upd = red_z && t.upd[r][E];
+  if (upd) sl[o + E] = v;
+  if (CHECK && upd && red_own && t.trow[r] && t.chk[E]) dmax = umax64(dmax, delta_bits(v, u));
+  return upd ? v : u;
 }
 
 template <typename R, bool CHECK>
-__global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
+__global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 5 : 8)
     k3d_tma(const __grid_constant__ CUtensorMap tm, R* __restrict__ dst, long long pitch, int nz, int ny, int nx,
             int zc, R w, IterCtl ctl) {
   extern __shared__ __align__(128) unsigned char t3_smem[];
@@ -185,29 +200,30 @@ __global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
   R* slot = reinterpret_cast<R*>(t3_smem);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(t3_smem + kT3NP * SP * sizeof(R));
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, half = (tid >> 4) & 1, p = tid & 15;
-  // ring-1 row of the thread: warp w holds rows base, base + 2 (one parity)
-  const int ty = (warp >> 1) * 4 + (warp & 1) + 2 * half;
+  const int p = tid & 15, rp = tid >> 4;  // column pair; rows 2rp, 2rp+1 of the ring-1 region
   const int x0 = 1 + (int)blockIdx.x * kT3X, y0 = 1 + (int)blockIdx.y * kT3Y;
   const int z0 = 1 + (int)blockIdx.z * zc, z1 = min(nz + 1, z0 + zc);  // owned planes [z0, z1)
-  const int wr = 1 + ty, wc = 2 + 2 * p;        // window row / first column of the pair
-  const int y = y0 - 2 + wr, xa = x0 - 3 + wc;  // global row / first column
+  const int wra = 1 + 2 * rp, wc = 2 + 2 * p;     // window row a (row b = wra + 1) / first column
+  const int ya = y0 - 2 + wra, xa = x0 - 3 + wc;  // global row a / first column
   T3Thread<R> t;
   // box origin: x0-3 rounded down to 16 B; the window starts xd columns into it
   const int xs = (x0 - 3) & ~(16 / (int)sizeof(R) - 1), xd = (x0 - 3) - xs;
-  t.off = wr * t3_wxb<R>() + wc + xd;
-  t.trow = wr >= 2 && wr < 2 + kT3Y;
-  const bool yin = y >= 1 && y <= ny;
+  t.off = wra * t3_wxb<R>() + wc + xd;
   const bool tcol0 = wc >= 3 && wc < 3 + kT3X, tcol1 = wc + 1 >= 3 && wc + 1 < 3 + kT3X;
-  t.upd[0] = yin && xa >= 1 && xa <= nx;
-  t.upd[1] = yin && xa + 1 >= 1 && xa + 1 <= nx;
   t.chk[0] = tcol0;
   t.chk[1] = tcol1;
-  {
-    const bool k0 = yin && tcol0 && xa >= 1 && xa <= nx, k1 = yin && tcol1 && xa + 1 <= nx;
-    t.st2 = k0 && k1 && (xa & 1) == 0;
-    t.st0 = k0 && !t.st2;
-    t.st1 = k1 && !t.st2;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int wr = wra + r, y = ya + r;
+    const bool yin = y >= 1 && y <= ny;
+    t.trow[r] = wr >= 2 && wr < 2 + kT3Y;
+    t.upd[r][0] = yin && xa >= 1 && xa <= nx;
+    t.upd[r][1] = yin && xa + 1 >= 1 && xa + 1 <= nx;
+    const bool k0 = t.trow[r] && yin && tcol0 && xa >= 1 && xa <= nx;
+    const bool k1 = t.trow[r] && yin && tcol1 && xa + 1 <= nx;
+    t.st2[r] = k0 && k1 && (xa & 1) == 0;
+    t.st0[r] = k0 && !t.st2[r];
+    t.st1[r] = k1 && !t.st2[r];
   }
   const uint32_t bar0 = smem_u32(bars);
   // Two planes per barrier.  The interval at z computes red(z), red(z+1) (old
@@ -229,17 +245,18 @@ __global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
   };
   if (tid == 0)  // planes 0..NP-4; interval q issues q+NP-4, q+NP-3 (into the slots of q-4, q-3)
     for (int q = 0; q < min(kT3NP - 3, nq); ++q) issue(q);
-  // the thread's reds (value after the red phase) of planes z-3, z-2, z-1
-  R r3 = R(0), r2 = R(0), r1 = R(0);
+  // the thread's reds (value after the red phase) of planes z-3, z-2, z-1, rows a, b
+  R r3a = R(0), r2a = R(0), r1a = R(0), r3b = R(0), r2b = R(0), r1b = R(0);
   unsigned long long dmax = 0ull;
   const long long zstride = (long long)(ny + 2) * pitch;
-  // pointer to the pair in plane z-2 of dst, advanced by two planes per interval
-  R* out = dst + (long long)(z0 - 3) * zstride + (long long)y * pitch + xa;
-  // the pair's red column in plane z0-1 (warp-uniform)
-  const int E0 = (z0 - 1 + y + xa) & 1;
+  // pointer to the pair of row a in plane z-2 of dst, advanced by two planes per interval
+  R* out = dst + (long long)(z0 - 3) * zstride + (long long)ya * pitch + xa;
+  // row a's red column in plane z0-1 (block-uniform; row b's is the other one)
+  const int E0 = (z0 - 1 + ya + xa) & 1;
   const int zr_lo = max(1, z0 - 1), zr_hi = min(nz, z1 + 1);  // planes with a red phase
   auto interval = [&](int z, auto e_const) {
-    constexpr int E = decltype(e_const)::value;  // red column of plane z
+    constexpr int E = decltype(e_const)::value;  // red column of row a in plane z
+    constexpr int F = E ^ 1;                     // ... of row b (and of row a in plane z+1)
     const int q = z - z0 + 2;
     __syncthreads();  // earlier reds are written; slots of planes z-4, z-3 are free
     if (tid == 0) {
@@ -258,58 +275,53 @@ __global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 4 : 5)
     R* sl[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) sl[k] = slot + ((q - 2 + k + kT3NP) % kT3NP) * SP;  // planes z-2 .. z+2
-    // Rows are loaded once per interval and shared between the phases that
-    // read them: slot z-1's own row is red(z)'s U and black(z-1)'s centre,
-    // slot z's own row is red(z)'s centre and red(z+1)'s U (column E^1, which
-    // red(z) does not write), slot z+1's own row is red(z)'s D and red(z+1)'s
-    // centre (read before red(z+1) writes its column).
-    const int o = t.off;
-    const T3Row<R> Bc = t3_row(sl[1], o);
-    const T3Row<R> Cn = t3_row(sl[2], o - WX), Cc = t3_row(sl[2], o), Cs = t3_row(sl[2], o + WX);
-    const T3Row<R> Dn = t3_row(sl[3], o - WX), Dc = t3_row(sl[3], o), Ds = t3_row(sl[3], o + WX);
-    const R Co = sl[2][o + (E == 0 ? -1 : 2)];
-    const R Do = sl[3][o + (E == 0 ? 2 : -1)];
-    const R Fc = sl[4][o + (E ^ 1)];
-    // red(z): column E
-    R rz = Cc.at(E);
-    {
-      const R v = t3_update<R, E>(Cn, Cc, Cs, Co, Bc.at(E), Dc.at(E), w);
-      const bool upd = (unsigned)(z - zr_lo) <= (unsigned)(zr_hi - zr_lo) && t.upd[E];
-      if (upd) {
-        sl[2][o + E] = v;
-        if (CHECK && z >= z0 && z < z1 && t.trow && t.chk[E]) dmax = umax64(dmax, delta_bits(v, rz));
-        rz = v;
-      }
+    // Rows are loaded once per interval and shared between the phases and the
+    // two rows that read them (see the 1-row notes: a row's red column is the
+    // only cell of it a red phase writes, and no phase reads that cell of a
+    // slot another phase of the interval writes).
+    const int oa = t.off, ob = oa + WX;
+    const bool rz_ok = (unsigned)(z - zr_lo) <= (unsigned)(zr_hi - zr_lo);
+    const bool rz1_ok = (unsigned)(z + 1 - zr_lo) <= (unsigned)(zr_hi - zr_lo);
+    const T3Row<R> Ba = t3_row(sl[1], oa), Bb = t3_row(sl[1], ob);
+    const T3Row<R> Cn = t3_row(sl[2], oa - WX), Ca = t3_row(sl[2], oa), Cb = t3_row(sl[2], ob),
+                   Cs = t3_row(sl[2], ob + WX);
+    const T3Row<R> Dn = t3_row(sl[3], oa - WX), Da = t3_row(sl[3], oa), Db = t3_row(sl[3], ob),
+                   Ds = t3_row(sl[3], ob + WX);
+    const R Fa = sl[4][oa + F], Fb = sl[4][ob + E];
+    const R Coa = sl[2][oa + (E == 0 ? -1 : 2)], Cob = sl[2][ob + (F == 0 ? -1 : 2)];
+    const R Doa = sl[3][oa + (F == 0 ? -1 : 2)], Dob = sl[3][ob + (E == 0 ? -1 : 2)];
+    // red(z): row a column E, row b column F
+    const R rza = t3_red<R, CHECK, E>(t, 0, rz_ok, z >= z0 && z < z1, w, sl[2], oa, Cn, Ca, Cb, Coa, Ba.at(E),
+                                      Da.at(E), dmax);
+    const R rzb = t3_red<R, CHECK, F>(t, 1, rz_ok, z >= z0 && z < z1, w, sl[2], ob, Ca, Cb, Cs, Cob, Bb.at(F),
+                                      Db.at(F), dmax);
+    // red(z+1): row a column F, row b column E
+    const R rz1a = t3_red<R, CHECK, F>(t, 0, rz1_ok, z + 1 >= z0 && z + 1 < z1, w, sl[3], oa, Dn, Da, Db, Doa,
+                                       Ca.at(F), Fa, dmax);
+    const R rz1b = t3_red<R, CHECK, E>(t, 1, rz1_ok, z + 1 >= z0 && z + 1 < z1, w, sl[3], ob, Da, Db, Ds, Dob,
+                                       Cb.at(E), Fb, dmax);
+    // black(z-2): row a column F, row b column E (the red columns of plane z-1); reds z-3, z-1
+    if (z - 2 >= z0 && z - 2 < z1) {
+      const T3Row<R> An = t3_row(sl[0], oa - WX), Aa = t3_row(sl[0], oa), Ab = t3_row(sl[0], ob),
+                     As = t3_row(sl[0], ob + WX);
+      const R Aoa = sl[0][oa + (F == 0 ? -1 : 2)], Aob = sl[0][ob + (E == 0 ? -1 : 2)];
+      t3_black<R, CHECK, F>(t, 0, w, An, Aa, Ab, Aoa, r3a, r1a, out, dmax);
+      t3_black<R, CHECK, E>(t, 1, w, Aa, Ab, As, Aob, r3b, r1b, out + pitch, dmax);
     }
-    // red(z+1): column E^1
-    R rz1 = Dc.at(E ^ 1);
-    {
-      const R v = t3_update<R, E ^ 1>(Dn, Dc, Ds, Do, Cc.at(E ^ 1), Fc, w);
-      const bool upd = (unsigned)(z + 1 - zr_lo) <= (unsigned)(zr_hi - zr_lo) && t.upd[E ^ 1];
-      if (upd) {
-        sl[3][o + (E ^ 1)] = v;
-        if (CHECK && z + 1 >= z0 && z + 1 < z1 && t.trow && t.chk[E ^ 1]) dmax = umax64(dmax, delta_bits(v, rz1));
-        rz1 = v;
-      }
-    }
-    if (t.trow) {
-      // black(z-2): column E^1 (red column of plane z-1), reds z-3, z-1
-      if (z - 2 >= z0 && z - 2 < z1) {
-        const T3Row<R> An = t3_row(sl[0], o - WX), Ac = t3_row(sl[0], o), As = t3_row(sl[0], o + WX);
-        const R Ao = sl[0][o + (E == 0 ? 2 : -1)];
-        t3_black<R, CHECK, E ^ 1>(t, w, An, Ac, As, Ao, r3, r1, out, dmax);
-      }
-      // black(z-1): column E, reds z-2, z
-      if (z - 1 >= z0 && z - 1 < z1) {
-        const T3Row<R> Bn = t3_row(sl[1], o - WX), Bs = t3_row(sl[1], o + WX);
-        const R Bo = sl[1][o + (E == 0 ? -1 : 2)];
-        t3_black<R, CHECK, E>(t, w, Bn, Bc, Bs, Bo, r2, rz, out + zstride, dmax);
-      }
+    // black(z-1): row a column E, row b column F; reds z-2, z
+    if (z - 1 >= z0 && z - 1 < z1) {
+      const T3Row<R> Bn = t3_row(sl[1], oa - WX), Bs = t3_row(sl[1], ob + WX);
+      const R Boa = sl[1][oa + (E == 0 ? -1 : 2)], Bob = sl[1][ob + (F == 0 ? -1 : 2)];
+      t3_black<R, CHECK, E>(t, 0, w, Bn, Ba, Bb, Boa, r2a, rza, out + zstride, dmax);
+      t3_black<R, CHECK, F>(t, 1, w, Ba, Bb, Bs, Bob, r2b, rzb, out + zstride + pitch, dmax);
     }
     out += 2 * zstride;
-    r3 = r1;
-    r2 = rz;
-    r1 = rz1;
+    r3a = r1a;
+    r2a = rza;
+    r1a = rz1a;
+    r3b = r1b;
+    r2b = rzb;
+    r1b = rz1b;
   };
   for (int z = z0 - 1; z - 2 <= z1 - 1; z += 2) {
     if (E0 == 0)
