@@ -1,5 +1,5 @@
 # K7 release variants on C2 (development aid)
-for i in 1 2; do for lib in libsor.so libsor_relonly.so libsor_fencerel.so; do
+for i in 1 2; do for lib in libsor.so libsor_relaxpoll.so; do
 SOR_LIBRARY=paper_1401_0763_b200/$lib python - <<'PY'
 import os,sys,torch
 sys.path.insert(0,'.')
