@@ -154,3 +154,37 @@ def test_resident_c1(gpu, orc):
         out = g.download()
     assert (r.converged, r.iters, r.max_change) == (True, rr.iters, rr.max_change) == (True, 1785, rr.max_change)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_resident_on_virtual_slabs_falls_back(gpu, orc, nslabs):
+    """SOR_KERNEL_RESIDENT on a multi-slab handle runs the slab path at depth T
+    (K7 needs one slab): bitwise, iterate and solve."""
+    init = _field(203, 150, seed=nslabs)
+    ref = init.copy()
+    rep = orc.iterate(ref, 1.9, 11, measure_last=True)
+    with gpu.Grid.create_virtual(init, nslabs) as g:
+        g.set_kernel("resident", 3)
+        d = g.iterate(1.9, 11, want_delta=True)
+        assert np.array_equal(g.download(), ref) and d == rep.max_change
+        r = g.solve(1.9, 1e-4, 400, 1)
+        rr = orc.solve(ref, 1.9, 1e-4, 400, 1)
+        assert (r.converged, r.iters, r.max_change) == (rr.converged, rr.iters, rr.max_change)
+        assert np.array_equal(g.download(), ref)
+
+
+def test_resident_on_external_stream(gpu, orc):
+    """K7 launches go to the handle's stream (an external torch stream here),
+    ordered with the caller's work on it."""
+    import torch
+    init = _field(613, 1029, seed=21)
+    ref = init.copy()
+    orc.iterate(ref, 1.8, 9)
+    s = torch.cuda.Stream()
+    with gpu.Grid.create(init) as g:
+        g.set_kernel("resident", 3)
+        g.set_stream(s.cuda_stream)
+        g.iterate(1.8, 9)
+        s.synchronize()
+        out = g.download()
+    assert np.array_equal(out, ref)
