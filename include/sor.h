@@ -62,7 +62,7 @@ typedef enum {
 
 /* Kernel variants (selected explicitly; there is no auto-dispatch).  All give
  * bitwise-identical results.                                  */
-#define SOR_MAX_T 4  /* deepest temporal blocking (iterations per HBM pass) */
+#define SOR_MAX_T 6  /* deepest temporal blocking (iterations per HBM pass); > 4: one slab, SOR only */
 
 typedef enum {
   SOR_KERNEL_NATURAL = 1,  /* K1: one launch per colour phase, in place, natural layout */
@@ -132,7 +132,9 @@ int sor_create_virtual(sor_grid** out, int64_t rows, int64_t cols, const double*
 
 /* Select the kernel variant.  temporal_depth T (iterations per HBM pass) is
  * used by SOR_KERNEL_TEMPORAL and SOR_KERNEL_RESIDENT, 1 <= T <= SOR_MAX_T
- * (T = 1 equals FUSED; multi-slab grids need slabs of >= 2T rows).
+ * (T = 1 equals FUSED; multi-slab grids need slabs of >= 2T rows; T = 5, 6
+ * only on single-slab handles (SOR_E_UNSUPPORTED otherwise), and Jacobi calls
+ * on a handle set deeper than 4 return SOR_E_UNSUPPORTED).
  * SOR_KERNEL_SMALL requires a single-slab grid that fits in shared memory;
  * SOR_KERNEL_NATURAL is not available on dist-IPC handles (SOR_E_UNSUPPORTED).
  * SOR_KERNEL_RESIDENT (K7, for small grids; the paper's per-phase barrier

@@ -494,7 +494,7 @@ int build(sor_grid* g, const std::vector<std::pair<int64_t, int64_t>>& spans, in
       g->slabs[k].ftop = f;
       g->slabs[k].fbot = f + g->nflags;
     }
-    g->H = 2 * kMaxT;
+    g->H = 2 * kMaxTLink;
   }
   if (g->mode == Mode::Virtual) {  // neighbours are the adjacent slabs
     const int n = (int)g->slabs.size();
@@ -1146,6 +1146,13 @@ int launch_wave(sor_grid* g, const Slab& s, int T, R w, const IterCtl& ctl, bool
     case 2: return launch_wave_L<R, 2, CK>(g, s, w, ctl, fused_fin);
     case 3: return launch_wave_L<R, 3, CK>(g, s, w, ctl, fused_fin);
     case 4: return launch_wave_L<R, 4, CK>(g, s, w, ctl, fused_fin);
+    // T > 4: the skew-2 kernel on one slab only (sor_set_kernel enforces it)
+    case 5:
+      if (!use_wave2(g, 5)) return set_error(nullptr, SOR_E_UNSUPPORTED, "T = 5 needs the skew-2 kernel (SOR_WAVE2)");
+      return launch_wave2_T<R, 5, CK, false>(g, s, w, ctl, fused_fin);
+    case 6:
+      if (!use_wave2(g, 6)) return set_error(nullptr, SOR_E_UNSUPPORTED, "T = 6 needs the skew-2 kernel (SOR_WAVE2)");
+      return launch_wave2_T<R, 6, CK, false>(g, s, w, ctl, fused_fin);
   }
   return set_error(nullptr, SOR_E_INVAL, "temporal depth %d unsupported", T);
 }
@@ -1393,7 +1400,7 @@ int enqueue_range(sor_grid* g, R w, int64_t k_from, int64_t k_to, const IterCtl&
         // K6: the full passes of an iterate block as one persistent launch
         // (all but a measured last pass)
         const int64_t full = left / T - ((check_last && end == k_to) ? 1 : 0);
-        if (full >= 2 && use_persist(g)) {
+        if (full >= 2 && T <= kMaxTLink && use_persist(g)) {
           const int rc = persist_passes<R>(g, w, T, (int)std::min<int64_t>(full, 1 << 20));
           if (rc == SOR_OK) {
             k += std::min<int64_t>(full, 1 << 20) * T;
@@ -1917,6 +1924,8 @@ int sor_set_kernel(sor_grid* g, int kernel, int temporal_depth) {
       if ((g->slabs.size() > 1 || g->nranks > 1) && thin < 2 * temporal_depth)
         return set_error(nullptr, SOR_E_INVAL, "slab of %lld rows too thin for T=%d", (long long)thin,
                          temporal_depth);
+      if (temporal_depth > kMaxTLink && !single_part(g))
+        return set_error(nullptr, SOR_E_UNSUPPORTED, "T > %d runs on single-slab handles only", kMaxTLink);
       g->kernel = kernel;
       g->tdepth = temporal_depth;
       break;
@@ -1981,6 +1990,8 @@ struct MethodGuard {  // run one call with the Jacobi method, then restore SOR
 int jacobi_usable(sor_grid* g) {
   if (g->kernel != SOR_KERNEL_FUSED && g->kernel != SOR_KERNEL_TEMPORAL && g->kernel != SOR_KERNEL_RESIDENT)
     return set_error(nullptr, SOR_E_UNSUPPORTED, "Jacobi runs on the FUSED / TEMPORAL / RESIDENT kernels only");
+  if (depth_of(g) > kMaxTLink)
+    return set_error(nullptr, SOR_E_UNSUPPORTED, "Jacobi runs at temporal depth <= %d", kMaxTLink);
   return SOR_OK;
 }
 }  // namespace

@@ -39,7 +39,8 @@ constexpr int kRowPad = 24;   // storage rows above/below a slab's owned rows + 
 constexpr int kWaveWarps = 4; // warps per CTA in wave_kernel (independent warps)
 constexpr int kWaveNC = 4;     // columns per lane in wave_kernel (strip = 32*kWaveNC columns)
 
-constexpr int kMaxT = 4;      // max temporal depth (iterations per HBM pass)
+constexpr int kMaxT = 6;      // max temporal depth (iterations per HBM pass; > kMaxTLink: one slab, SOR only)
+constexpr int kMaxTLink = 4;  // max depth of multi-slab handles, Jacobi and the skew-1 / persistent kernels
 
 // Wave-kernel build options (A/B experiments; the defaults are the product):
 // SOR_WAVE_HOIST issues every stage's lane-neighbour shuffle at the start of

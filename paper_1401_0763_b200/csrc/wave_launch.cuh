@@ -122,7 +122,7 @@ int launch_wave2_T(sor_grid* g, const Slab& s, R w, const IterCtl& ctl, bool fus
   // a deeper TMA look-ahead pays for one-wave launches at T = 4 (C3-sized
   // slabs); multi-wave launches (C4, C5) and T < 4 keep the smaller ring
   const double cells = (double)(s.g_hi - s.g_lo) * (double)g->cols;
-  if (T == 4 && cells <= 64.0 * (1 << 20)) return launch_wave2_TR<R, T, CK, LINK, 3>(g, s, w, ctl, fused_fin);
+  if (T >= 4 && cells <= 64.0 * (1 << 20)) return launch_wave2_TR<R, T, CK, LINK, 3>(g, s, w, ctl, fused_fin);
   return launch_wave2_TR<R, T, CK, LINK, 2>(g, s, w, ctl, fused_fin);
 }
 
