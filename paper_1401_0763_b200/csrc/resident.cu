@@ -108,7 +108,12 @@ int res_launch(sor_grid* g, const ResPlan& p, const ResArgs<R>& a, bool coop) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = coop ? 1 : 0;
-  CU(cudaLaunchKernelEx(&cfg, kern, a));
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (coop && e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();  // not all blocks can be resident now: the caller falls back to the wave path
+    return SOR_E_UNSUPPORTED;
+  }
+  CU(e);
   g->st.kernel_launches += 1;
   return SOR_OK;
 }

@@ -193,10 +193,13 @@ int launch_wave_persist_S(sor_grid* g, const Slab& s, R w, int npasses, unsigned
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (W2)
-    CU(cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap2[p0], s.tmap2[p1]));
-  else
-    CU(cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap[p0], s.tmap[p1]));
+  const cudaError_t e = W2 ? cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap2[p0], s.tmap2[p1])
+                           : cudaLaunchKernelEx(&cfg, kern, a, npasses, gbar, s.tmap[p0], s.tmap[p1]);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();  // not co-resident now (other work on the device): pass-by-pass launches instead
+    return SOR_E_UNSUPPORTED;
+  }
+  CU(e);
   g->st.kernel_launches += 1;
   return SOR_OK;
 }
