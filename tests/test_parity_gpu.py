@@ -187,7 +187,7 @@ def test_invalid_calls_leave_handle_usable(gpu):
     with gpu.Grid.create(init) as g:
         for bad in (lambda: g.iterate(2.0, 1), lambda: g.iterate(0.0, 1), lambda: g.iterate(1.0, -1),
                     lambda: g.solve(1.5, 0.0, 10), lambda: g.solve(1.5, 1e-3, 10, 11),
-                    lambda: g.set_kernel("temporal", 5), lambda: g.set_kernel(99)):
+                    lambda: g.set_kernel("temporal", 7), lambda: g.set_kernel(99)):
             with pytest.raises(gpu.SorError) as e:
                 bad()
             assert e.value.code == gpu.SOR_E_INVAL
