@@ -92,6 +92,10 @@ def lib():
             f.restype = i32
             f.argtypes = [vp, i64, i64, i64, dbl, i32, i64, dbl, i64, i32, rp]
         _lib.orc_dense_solve3d_f64.restype = i32
+        for name in ("orc_variant_run_f64", "orc_variant_run_f32"):
+            f = getattr(_lib, name)
+            f.restype = i32
+            f.argtypes = [vp, i64, i64, i32, i64, i64, i64, dbl, i32, i64, dbl, i64, i32, rp]
         _lib.orc_dense_solve3d_f64.argtypes = [vp, i64, i64, i64]
         _lib.orc_jacobi_f64.restype = i32
         _lib.orc_jacobi_f64.argtypes = [vp, i64, i64, i64, dbl, rp]
@@ -222,6 +226,38 @@ def sor3d_iterate(u: np.ndarray, omega: float, iters: int, measure_last: bool = 
 
 def sor3d_solve(u: np.ndarray, omega: float, tol: float, maxit: int, check_every: int = 1) -> Report:
     return _sor3d(u, omega, 1, maxit, tol, check_every, False)
+
+
+def _variant(u, kind, p1, p2, p3, omega, mode, n_iter, tol, K, measure_last) -> Report:
+    f64 = u.dtype == np.float64
+    _grid(u, np.float64 if f64 else np.float32)
+    r = _Report()
+    fn = lib().orc_variant_run_f64 if f64 else lib().orc_variant_run_f32
+    fn(u.ctypes.data, u.shape[0] - 2, u.shape[1] - 2, kind, p1, p2, p3, omega, mode, n_iter, tol, K,
+       int(measure_last), ctypes.byref(r))
+    if r.status < 0:
+        raise ValueError("oracle rejected arguments")
+    return _rep(r)
+
+
+def multicolor_iterate(u: np.ndarray, omega: float, iters: int, ca: int = 1, cb: int = 1, nc: int = 2,
+                       measure_last: bool = False) -> Report:
+    """NEXT-4 (reading N4-1): multi-colour SOR, colour (ca*i + cb*j) mod nc, phases 0..nc-1."""
+    return _variant(u, 0, ca, cb, nc, omega, 0, iters, 1.0, 1, measure_last)
+
+
+def multicolor_solve(u: np.ndarray, omega: float, tol: float, maxit: int, check_every: int = 1,
+                     ca: int = 1, cb: int = 1, nc: int = 2) -> Report:
+    return _variant(u, 0, ca, cb, nc, omega, 1, maxit, tol, check_every, False)
+
+
+def block_iterate(u: np.ndarray, omega: float, iters: int, block: int, measure_last: bool = False) -> Report:
+    """NEXT-4 (reading N4-2): block red-black SOR, natural order inside block x block blocks."""
+    return _variant(u, 1, block, 0, 0, omega, 0, iters, 1.0, 1, measure_last)
+
+
+def block_solve(u: np.ndarray, omega: float, tol: float, maxit: int, block: int, check_every: int = 1) -> Report:
+    return _variant(u, 1, block, 0, 0, omega, 1, maxit, tol, check_every, False)
 
 
 def dense_solve3d(u: np.ndarray) -> None:

@@ -553,3 +553,99 @@ int orc_dense_solve3d_f64(double* u, int64_t nz, int64_t ny, int64_t nx) {
   free(A);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the two parallel SOR variants the paper names beside
+ * red-black SOR, "multi-color SOR" and "block-parallel SOR".  The paper only
+ * names them; the definitions below are readings N4-1 and N4-2 of DESIGN.md
+ * §3 (the textbook orderings), written out plainly.  Every update is Eq. 1
+ * in the canonical order of orc_cell_update (readings #2-#4),
+ * in place, reading the latest values; |delta| = |u' - u| (reading #5);
+ * Algorithm 1's loop, cadence and strict stop test as orc_sor_run.
+ *
+ * Multi-colour (N4-1): colour(i, j) = (ca*i + cb*j) mod nc (storage indices,
+ * 1..rows x 1..cols; non-negative residue).  Valid iff ca, cb are not
+ * multiples of nc, so 5-point neighbours never share a colour.  One
+ * iteration = phases p = 0, 1, ..., nc-1; phase p updates every cell of
+ * colour p.  (ca, cb, nc) = (1, 1, 2) is the paper's red-black SOR
+ * (P:149).
+ *
+ * Block (N4-2): the interior is cut into B x B blocks anchored at cell (1, 1)
+ * (block (bi, bj) = ((i-1)/B, (j-1)/B), clipped at the edges); blocks are
+ * coloured like a chessboard, red iff bi+bj even.  One iteration = the red
+ * blocks, then the black blocks; inside a block the cells are updated in
+ * natural (lexicographic) order, as Code 1's sequential sweep.
+ * B = 1 is red-black SOR; B >= max(rows, cols) is natural-order SOR.        */
+static int64_t mc_colour(int64_t ca, int64_t cb, int64_t nc, int64_t i, int64_t j) {
+  int64_t c = (ca * i + cb * j) % nc;
+  return c < 0 ? c + nc : c;
+}
+
+#define DEFINE_VARIANTS(T, SUF, ABS)                                                   \
+  static void cell_##SUF(T* u, int64_t ld, int64_t i, int64_t j, T w, int check, T* m) { \
+    const T q = (T)0.25;                                                              \
+    T* uc = u + i * ld + j;                                                           \
+    T s = (uc[-ld] + uc[ld]) + (uc[-1] + uc[1]);                                      \
+    T a = q * s;                                                                      \
+    T r = a - uc[0];                                                                  \
+    T un = uc[0] + w * r;                                                             \
+    if (check) {                                                                      \
+      T d = ABS(un - uc[0]);                                                          \
+      if (d > *m || d != d) *m = d;                                                   \
+    }                                                                                 \
+    uc[0] = un;                                                                       \
+  }                                                                                   \
+  /* kind 0: multi-colour (p1, p2, p3) = (ca, cb, nc); kind 1: block, p1 = B */      \
+  int orc_variant_run_##SUF(T* u, int64_t rows, int64_t cols, int kind, int64_t p1,   \
+                            int64_t p2, int64_t p3, double omega, int mode,           \
+                            int64_t n_iter, double tol, int64_t K, int measure_last,  \
+                            orc_report* rep) {                                        \
+    memset(rep, 0, sizeof(*rep));                                                     \
+    int ok = check_args(rows, cols, omega, mode, n_iter, tol, K);                     \
+    if (kind == 0) ok = ok && p3 >= 2 && p1 % p3 != 0 && p2 % p3 != 0;                \
+    else if (kind == 1) ok = ok && p1 >= 1;                                           \
+    else ok = 0;                                                                      \
+    if (!ok) {                                                                        \
+      rep->status = ORC_E_INVAL;                                                      \
+      return ORC_E_INVAL;                                                             \
+    }                                                                                 \
+    const int64_t ld = cols + 2;                                                      \
+    const T w = (T)omega;                                                             \
+    rep->status = mode == 1 ? ORC_NOT_CONVERGED : ORC_DONE;                           \
+    for (int64_t k = 1; k <= n_iter; ++k) {                    /* P:301 */            \
+      int check = mode == 1 ? (k % K == 0) : (measure_last && k == n_iter);           \
+      T m = (T)0;                                                                     \
+      if (kind == 0) {                                                                \
+        for (int64_t p = 0; p < p3; ++p) {                     /* colour phases */    \
+          for (int64_t i = 1; i <= rows; ++i)                                         \
+            for (int64_t j = 1; j <= cols; ++j)                                       \
+              if (mc_colour(p1, p2, p3, i, j) == p) cell_##SUF(u, ld, i, j, w, check, &m); \
+          rep->half_sweeps += 1;                                                      \
+        }                                                                             \
+      } else {                                                                        \
+        const int64_t B = p1, nbi = (rows + B - 1) / B, nbj = (cols + B - 1) / B;      \
+        for (int c = 0; c < 2; ++c) {                          /* red, then black */  \
+          for (int64_t bi = 0; bi < nbi; ++bi)                                        \
+            for (int64_t bj = 0; bj < nbj; ++bj) {                                    \
+              if ((bi + bj) % 2 != c) continue;                                       \
+              for (int64_t i = 1 + bi * B; i <= rows && i < 1 + (bi + 1) * B; ++i)    \
+                for (int64_t j = 1 + bj * B; j <= cols && j < 1 + (bj + 1) * B; ++j)  \
+                  cell_##SUF(u, ld, i, j, w, check, &m);                              \
+            }                                                                         \
+          rep->half_sweeps += 1;                                                      \
+        }                                                                             \
+      }                                                                               \
+      rep->iters = k;                                                                 \
+      if (check) {                                                                    \
+        rep->checks += 1;                                                             \
+        rep->max_change = (double)m;                                                  \
+        if (mode == 1 && (double)m < tol) {                    /* P:327 */            \
+          rep->status = ORC_DONE;                                                     \
+          break;                                                                      \
+        }                                                                             \
+      }                                                                               \
+    }                                                                                 \
+    return rep->status;                                                               \
+  }
+DEFINE_VARIANTS(double, f64, fabs)
+DEFINE_VARIANTS(float, f32, fabsf)

@@ -108,6 +108,19 @@ int orc_sor3d_run_f64(double* u, int64_t nz, int64_t ny, int64_t nx, double omeg
 int orc_sor3d_run_f32(float* u, int64_t nz, int64_t ny, int64_t nx, double omega, int mode,
                       int64_t n_iter, double tol, int64_t K, int measure_last, orc_report* rep);
 
+/* NEXT-4 (readings N4-1, N4-2): multi-colour SOR (kind 0: colour
+ * (p1*i + p2*j) mod p3, phases 0..p3-1; p1, p2 not multiples of p3) and
+ * block red-black SOR (kind 1: p1 x p1 blocks, chessboard of blocks, red
+ * first, natural order inside a block).  Modes, cadence, |delta| and the
+ * stop test as orc_sor_run; half_sweeps counts colour phases (p3 or 2 per
+ * iteration).  f32: float storage and arithmetic.                          */
+int orc_variant_run_f64(double* u, int64_t rows, int64_t cols, int kind, int64_t p1, int64_t p2,
+                        int64_t p3, double omega, int mode, int64_t n_iter, double tol, int64_t K,
+                        int measure_last, orc_report* rep);
+int orc_variant_run_f32(float* u, int64_t rows, int64_t cols, int kind, int64_t p1, int64_t p2,
+                        int64_t p3, double omega, int mode, int64_t n_iter, double tol, int64_t K,
+                        int measure_last, orc_report* rep);
+
 /* Brute force for the 3-D pin (test only): the 7-point Dirichlet system by
  * dense Gaussian elimination; nz*ny*nx <= 1728.                             */
 int orc_dense_solve3d_f64(double* u, int64_t nz, int64_t ny, int64_t nx);
