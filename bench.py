@@ -242,9 +242,10 @@ def cpu_baseline(cfg, window):
 
 # ------------------------------------------------------------------ NEXT rows
 def run_next(args):
-    """NEXT-2 (Jacobi on C3's grid, 1000 iterations, T-deep passes) and NEXT-3
-    (3-D SOR, 512^3 fp64, 50 iterations, two-pass colour phases): the same
-    JSON contract as the headline line, one GPU."""
+    """NEXT-2 (Jacobi on C3's grid, 1000 iterations, T-deep passes), NEXT-3
+    (3-D SOR, 512^3 fp64, 50 iterations) and NEXT-4 (multi-colour / block
+    red-black SOR on C3's grid, 200 iterations): the same JSON contract as the
+    headline line, one GPU."""
     import torch
 
     import oracle
@@ -263,6 +264,26 @@ def run_next(args):
         reset_d = lambda: g.reset(torch.from_numpy(init_h).cuda())  # noqa: E731
         bytes_per_update = 16.0 / T
         kname, workload = f"jacobi_kernel<f64,T={T},ck=0>", f"Jacobi (NEXT-2) on the C3 grid: 4096x4096 f64, {iters} iterations"
+        elapsed = lambda: g.elapsed_ms                     # noqa: E731
+        launches = lambda: g.stats["kernel_launches"]      # noqa: E731
+    elif args.method in ("multicolor", "block"):
+        cfg = SI.config("C3")
+        init_h = cfg.init()
+        iters, units = 200, cfg.rows * cfg.cols
+        if args.method == "multicolor":
+            ca, cb, nc = (int(x) for x in args.colours.split(","))
+            var = P.Variant.multicolor(ca, cb, nc)
+            kname = f"mc_kernel<f64> (colour ({ca}i+{cb}j) mod {nc}, {nc} phases in shared memory)"
+            vdesc = f"multi-colour SOR (NEXT-4, reading N4-1), colour ({ca}i+{cb}j) mod {nc}"
+        else:
+            var = P.Variant.blocks(args.block)
+            kname = f"bp_kernel<f64> (block {args.block}, red/black blocks in shared memory)"
+            vdesc = f"block red-black SOR (NEXT-4, reading N4-2), {args.block}x{args.block} blocks"
+        g = P.Grid.create(torch.from_numpy(init_h).cuda())
+        run = lambda n: g.variant_iterate(var, cfg.omega, n)  # noqa: E731
+        reset_d = lambda: g.reset(torch.from_numpy(init_h).cuda())  # noqa: E731
+        bytes_per_update = 16.0
+        workload = f"{vdesc} on the C3 grid: 4096x4096 f64, omega_opt, {iters} iterations"
         elapsed = lambda: g.elapsed_ms                     # noqa: E731
         launches = lambda: g.stats["kernel_launches"]      # noqa: E731
     else:
@@ -318,6 +339,10 @@ def run_next(args):
             g.reset(hin)
             g.jacobi(iters)
             g.download(hout)
+        elif args.method in ("multicolor", "block"):
+            g.reset(hin)
+            run(iters)
+            g.download(hout)
         else:
             g3 = P.Grid3D(hin.numpy())
             g3.set_kernel(k3)
@@ -333,9 +358,13 @@ def run_next(args):
     while time.perf_counter() - t0 < args.cpu_budget:
         if args.method == "jacobi":
             oracle.jacobi_iterate(u, 2)
+        elif args.method == "multicolor":
+            oracle.multicolor_iterate(u, cfg.omega, 2, ca, cb, nc)
+        elif args.method == "block":
+            oracle.block_iterate(u, cfg.omega, 2, args.block)
         else:
             oracle.sor3d_iterate(u, 1.9, 1)
-        k += 2 if args.method == "jacobi" else 1
+        k += 1 if args.method == "sor3d" else 2
     tc = time.perf_counter() - t0
     line["cpu_baseline"] = {"value": units * k / tc / 1e9, "unit": "GLUP/s", "cores": 1, "kind": "oracle",
                             "sample": f"first {k} iterations of the same grid, single-thread oracle, {tc:.1f} s"}
@@ -488,8 +517,11 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (32768^2) sub-record")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 (latency configs) sub-record")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--method", default="sor", choices=["sor", "jacobi", "sor3d"],
-                    help="sor: the headline path; jacobi / sor3d: the NEXT-2 / NEXT-3 rows (1 GPU)")
+    ap.add_argument("--method", default="sor", choices=["sor", "jacobi", "sor3d", "multicolor", "block"],
+                    help="sor: the headline path; jacobi / sor3d / multicolor, block: the NEXT-2 / NEXT-3 / "
+                         "NEXT-4 rows (1 GPU)")
+    ap.add_argument("--colours", default="1,1,4", help="multicolor: ca,cb,nc (colour (ca*i+cb*j) mod nc)")
+    ap.add_argument("--block", type=int, default=8, help="block: block side B")
     args = ap.parse_args()
     if args.dtype is None:
         args.dtype = "f32" if args.config == "C4F32" else "f64"

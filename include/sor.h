@@ -176,6 +176,34 @@ int sor_jacobi_iterate(sor_grid* g, int64_t iters, double* last_max_change);
 int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
                      double* max_change_out);
 
+/* NEXT-4: the parallel SOR variants the paper names beside red-black SOR
+ * [§3.1, P:147] ("multi-color SOR", "block-parallel SOR"; no algorithm is
+ * given there: DESIGN.md §3 readings N4-1 / N4-2 define them), on the same
+ * handle and layout.  Every update is Eq. 1 [P:97-100] in the canonical
+ * order, in place, reading the latest values.
+ *   SOR_VARIANT_MULTICOLOR: colour(i, j) = (ca*i + cb*j) mod nc (storage
+ *     indices, non-negative residue); one iteration = colour phases 0, 1,
+ *     ..., nc-1.  Needs 2 <= nc <= 8 (else SOR_E_UNSUPPORTED) and ca, cb not
+ *     multiples of nc (else SOR_E_INVAL: 5-point neighbours would share a
+ *     colour).  (1, 1, 2) is red-black SOR.
+ *   SOR_VARIANT_BLOCK: block x block blocks anchored at cell (1, 1), red iff
+ *     bi+bj even; the red blocks, then the black blocks, natural (row-major)
+ *     order inside a block.  Needs 1 <= block <= 32 (else
+ *     SOR_E_UNSUPPORTED).  block = 1 is red-black SOR.
+ * Single-GPU handles only (virtual / dist: SOR_E_UNSUPPORTED); the handle's
+ * sor_kernel setting is not used.  Contracts, outputs and errors otherwise as
+ * sor_iterate / sor_solve; `v` is read during the call only.  Stats:
+ * half_sweeps counts colour phases (nc or 2 per iteration).                */
+typedef enum { SOR_VARIANT_MULTICOLOR = 1, SOR_VARIANT_BLOCK = 2 } sor_variant_kind;
+typedef struct {
+  int32_t kind;       /* sor_variant_kind                    */
+  int32_t ca, cb, nc; /* multi-colour: colour (ca*i+cb*j) mod nc */
+  int32_t block;      /* block: block side B                 */
+} sor_variant;
+int sor_variant_iterate(sor_grid* g, const sor_variant* v, double omega, int64_t iters, double* last_max_change);
+int sor_variant_solve(sor_grid* g, const sor_variant* v, double omega, double tol, int64_t maxit,
+                      int64_t check_every, int64_t* iters_out, double* max_change_out);
+
 /* 3-D red-black SOR (NEXT-3; the paper's future work): a separate
  * single-GPU handle over an nz x ny x nx interior with a Dirichlet shell.
  * `init` = caller-owned (nz+2)*(ny+2)*(nx+2) fp64 array, row-major with z

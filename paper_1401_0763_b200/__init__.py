@@ -33,7 +33,22 @@ EXPORTS = ("sor_create", "sor_create_rect", "sor_create_dist", "sor_nccl_unique_
            "sor_download_rows", "sor_reset", "sor_set_stream", "sor_last_elapsed_ms", "sor_get_stats",
            "sor_partition_rows", "sor_destroy", "sor_last_error", "sor_jacobi_iterate", "sor_jacobi_solve",
            "sor3d_create", "sor3d_iterate", "sor3d_solve", "sor3d_download", "sor3d_last_elapsed_ms",
-           "sor3d_destroy", "sor3d_set_kernel")
+           "sor3d_destroy", "sor3d_set_kernel", "sor_variant_iterate", "sor_variant_solve")
+VARIANT_MULTICOLOR, VARIANT_BLOCK = 1, 2
+
+
+class Variant(ctypes.Structure):
+    """sor_variant (include/sor.h): NEXT-4 multi-colour / block red-black SOR."""
+    _fields_ = [("kind", ctypes.c_int32), ("ca", ctypes.c_int32), ("cb", ctypes.c_int32),
+                ("nc", ctypes.c_int32), ("block", ctypes.c_int32)]
+
+    @classmethod
+    def multicolor(cls, ca: int = 1, cb: int = 1, nc: int = 2) -> "Variant":
+        return cls(VARIANT_MULTICOLOR, ca, cb, nc, 0)
+
+    @classmethod
+    def blocks(cls, block: int) -> "Variant":
+        return cls(VARIANT_BLOCK, 0, 0, 0, block)
 
 
 class SorError(RuntimeError):
@@ -99,6 +114,9 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         "sor3d_last_elapsed_ms": (i32, [vp, ctypes.POINTER(dbl)]),
         "sor3d_destroy": (None, [vp]),
         "sor3d_set_kernel": (i32, [vp, i32]),
+        "sor_variant_iterate": (i32, [vp, ctypes.POINTER(Variant), dbl, i64, ctypes.POINTER(dbl)]),
+        "sor_variant_solve": (i32, [vp, ctypes.POINTER(Variant), dbl, dbl, i64, i64, ctypes.POINTER(i64),
+                                    ctypes.POINTER(dbl)]),
         "sor_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -270,6 +288,20 @@ class Grid:
         it, m = ctypes.c_int64(0), ctypes.c_double(0.0)
         rc = _check(lib().sor_jacobi_solve(self._h, tol, maxit, check_every, ctypes.byref(it), ctypes.byref(m)),
                     allow_not_converged=True)
+        return SolveResult(rc == SOR_OK, it.value, m.value)
+
+    def variant_iterate(self, variant: "Variant", omega: float, iters: int, want_delta: bool = False):
+        """NEXT-4: `iters` iterations of a multi-colour / block SOR variant."""
+        d = ctypes.c_double()
+        _check(lib().sor_variant_iterate(self._h, ctypes.byref(variant), omega, iters,
+                                         ctypes.byref(d) if want_delta else None))
+        return d.value if want_delta else None
+
+    def variant_solve(self, variant: "Variant", omega: float, tol: float, maxit: int,
+                      check_every: int = 1) -> SolveResult:
+        it, m = ctypes.c_int64(0), ctypes.c_double(0.0)
+        rc = _check(lib().sor_variant_solve(self._h, ctypes.byref(variant), omega, tol, maxit, check_every,
+                                            ctypes.byref(it), ctypes.byref(m)), allow_not_converged=True)
         return SolveResult(rc == SOR_OK, it.value, m.value)
 
     def _receives(self) -> bool:

@@ -418,6 +418,8 @@ void free_grid(sor_grid* g) {
   if (g->rflags) cudaFree(g->rflags);
   if (g->flagbuf) cudaFree(g->flagbuf);
   if (g->djoin) cudaFree(g->djoin);
+  if (g->vctl) cudaFree(g->vctl);
+  if (g->vhost) cudaFreeHost(g->vhost);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   for (int k = 0; k < 2; ++k)
@@ -2018,6 +2020,47 @@ int sor_jacobi_solve(sor_grid* g, double tol, int64_t maxit, int64_t check_every
   MethodGuard mg(g);
   if (g->dt == SOR_F64) return solve_impl<double>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
   return solve_impl<float>(g, 1.0, tol, maxit, check_every, iters_out, max_change_out);
+}
+
+int sor_variant_iterate(sor_grid* g, const sor_variant* v, double omega, int64_t iters, double* last_max_change) {
+  TRY(usable(g));
+  TRY(validate_omega(omega));
+  if (iters < 0) return set_error(nullptr, SOR_E_INVAL, "iters must be >= 0");
+  TRY(variant_check(g, v));
+  DevGuard dg(g);
+  TRY(begin_call(g));
+  double m = 0.0;
+  const int rc = g->dt == SOR_F64
+                     ? variant_run<double>(g, v, omega, 0, iters, 1.0, 1, last_max_change != nullptr, nullptr, &m, nullptr)
+                     : variant_run<float>(g, v, omega, 0, iters, 1.0, 1, last_max_change != nullptr, nullptr, &m, nullptr);
+  if (rc < 0) return rc;
+  TRY(end_call(g, nullptr));
+  if (last_max_change) *last_max_change = iters > 0 ? m : 0.0;
+  return SOR_OK;
+}
+
+int sor_variant_solve(sor_grid* g, const sor_variant* v, double omega, double tol, int64_t maxit,
+                      int64_t check_every, int64_t* iters_out, double* max_change_out) {
+  TRY(usable(g));
+  TRY(validate_omega(omega));
+  if (!(tol > 0.0) || !std::isfinite(tol)) return set_error(nullptr, SOR_E_INVAL, "tol must be finite and > 0");
+  if (maxit < 1) return set_error(nullptr, SOR_E_INVAL, "maxit must be >= 1");
+  if (check_every < 1 || check_every > maxit)
+    return set_error(nullptr, SOR_E_INVAL, "need 1 <= check_every <= maxit (S:114)");
+  TRY(variant_check(g, v));
+  DevGuard dg(g);
+  TRY(begin_call(g));
+  int64_t it = 0;
+  double m = 0.0;
+  int conv = 0;
+  const int rc = g->dt == SOR_F64
+                     ? variant_run<double>(g, v, omega, 1, maxit, tol, check_every, 0, &it, &m, &conv)
+                     : variant_run<float>(g, v, omega, 1, maxit, tol, check_every, 0, &it, &m, &conv);
+  if (rc < 0) return rc;
+  TRY(end_call(g, nullptr));
+  if (iters_out) *iters_out = it;
+  if (max_change_out) *max_change_out = m;
+  return conv ? SOR_OK : SOR_NOT_CONVERGED;
 }
 
 int sor_download(sor_grid* g, double* out) {

@@ -125,6 +125,8 @@ struct sor_grid {
   int64_t exact_reruns = 0;  // solve passes re-run with exact maxima (diagnostic)
   int every_ck = 4;          // max-change mode of T-deep solve passes with check_every == 1
   int method = 0;            // 0: red-black SOR; 1: Jacobi (sor_jacobi_*; NEXT-2)
+  void* vctl = nullptr;      // NEXT-4 variants: device control block (variants.cu)
+  void* vhost = nullptr;     // ... and its pinned host copy
   bool failed = false;
   bool have_elapsed = false;
   double elapsed_ms = 0.0;
@@ -200,5 +202,12 @@ int launch_resident_iterate(sor_grid* g, R w, int64_t iters, int T, bool check_l
 template <typename R>
 int launch_resident_single(sor_grid* g, R w, int solve, int64_t n_iter, double tol, int64_t K, int check_last);
 bool resident_fits(const sor_grid* g, int T, bool single);
+
+// NEXT-4 (variants.cu): multi-colour / block red-black SOR on single-GPU
+// handles, one HBM pass per iteration.
+int variant_check(const sor_grid* g, const sor_variant* v);
+template <typename R>
+int variant_run(sor_grid* g, const sor_variant* v, double omega, int solve, int64_t n_iter, double tol, int64_t K,
+                int measure_last, int64_t* iters_out, double* max_out, int* converged);
 
 }  // namespace sorh
