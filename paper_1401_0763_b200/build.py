@@ -63,8 +63,14 @@ def build_lib(force: bool = False, verbose: bool = False, out: str = LIB, define
     inc = ["-I" + INCLUDE, "-I" + os.path.join(nc, "include")]
     dflags = ["-D" + d for d in defines]
 
+    hdr_mtime = max(os.path.getmtime(h) for h in sources() if not h.endswith(".cu"))
+
     def compile_one(src: str) -> str:
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        # incremental (not forced): a unit is rebuilt if it or any header is newer than its object
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_mtime)):
+            return obj
         cmd = [NVCC, *NVCC_FLAGS, *dflags, *inc, "-c", src, "-o", obj + ".tmp"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
