@@ -231,7 +231,9 @@ __global__ void __launch_bounds__(kT3Threads, sizeof(R) == 8 ? 5 : 8)
   // written in earlier intervals; the vertical reds are the thread's own).
   // Intervals z = z0-1, z0+1, ... while z-2 <= z1-1; planes z0-2 .. z+2.
   const int nint = (z1 + 1 - (z0 - 1)) / 2 + 1;
-  const int nq = 2 * nint + 3;  // planes q = z - z0 + 2 in [0, nq)
+  // planes q = z - z0 + 2 in [0, nq): the last interval (q = 2 nint - 1) reads
+  // up to q + 2, and every issued plane is waited for before the CTA exits
+  const int nq = 2 * nint + 2;
   if (tid == 0) {
     for (int s = 0; s < kT3NP; ++s) mbar_init(bar0 + 8u * s, 1);
     mbar_fence_init();
