@@ -168,6 +168,34 @@ def test_device_pointers_and_reset(gpu, orc):
     assert np.array_equal(rows, ref[50:61])
 
 
+def test_device_init_written_by_pending_gpu_work(gpu, orc):
+    """A device-resident init is read after the caller's pending work on other
+    streams (sor.h: create / reset order their reads after it): the tensor is
+    filled by asynchronous GPU work queued behind ~10 ms of kernels, and create
+    / reset are called at once."""
+    import torch
+    init = SI.random_edges(300, 517, seed=21)
+    ref = init.copy()
+    orc.iterate(ref, 1.7, 9)
+    pinned = torch.from_numpy(init).pin_memory()
+    ballast = torch.empty(1 << 27, dtype=torch.float32, device="cuda")
+    for use_reset in (False, True):
+        dinit = torch.zeros(init.shape, dtype=torch.float64, device="cuda")
+        g0 = gpu.Grid.create(np.zeros_like(init)) if use_reset else None
+        torch.cuda.synchronize()
+        for _ in range(12):
+            ballast.normal_()                       # keeps the current stream busy
+        dinit.copy_(pinned, non_blocking=True)      # the fill, queued behind it
+        g = g0 if use_reset else gpu.Grid.create(dinit)
+        if use_reset:
+            g.reset(dinit)
+        with g:
+            g.set_kernel("temporal", 3)
+            g.iterate(1.7, 9)
+            out = g.download()
+        assert np.array_equal(out, ref), use_reset
+
+
 def test_external_stream(gpu, orc):
     import torch
     init = SI.random_edges(64, 300, seed=2)
