@@ -109,3 +109,41 @@ def test_device_copies_are_stream_ordered():
     src = "".join(open(f).read() for f in glob.glob(os.path.join(ROOT, "paper_1401_0763_b200", "csrc", "*.cu")))
     assert not re.findall(r"\bcudaMemcpy(?:2D)?\(", src)
     assert not re.findall(r"\bcudaMemset\(", src)
+
+
+def test_binding_rejects_wrong_buffers_before_the_c_call():
+    """The binding checks dtype, contiguity and the exact shape of every grid
+    buffer before handing a raw pointer to C (a wrong size there is an
+    out-of-bounds access), and maps dtype names explicitly."""
+    import numpy as np
+    good = np.zeros((6, 9))
+    assert P._ptr(good, shape=(6, 9))[0] == good.ctypes.data
+    with pytest.raises(ValueError):
+        P._ptr(good, shape=(9, 6))
+    with pytest.raises(ValueError):
+        P._ptr(np.zeros(54), shape=(6, 9))
+    with pytest.raises(TypeError):
+        P._ptr(np.zeros((6, 9), dtype=np.float32), shape=(6, 9))
+    with pytest.raises(TypeError):
+        P._ptr(np.zeros((9, 6)).T, shape=(6, 9))            # not C-contiguous
+    ro = np.zeros((6, 9))
+    ro.flags.writeable = False
+    with pytest.raises(TypeError):
+        P._ptr(ro, writable=True, shape=(6, 9))
+    with pytest.raises(TypeError):
+        P._ptr([[0.0] * 9] * 6, shape=(6, 9))
+    import torch
+    t = torch.zeros(6, 9, dtype=torch.float64)
+    assert P._ptr(t, shape=(6, 9))[0] == t.data_ptr()
+    with pytest.raises(ValueError):
+        P._ptr(t, shape=(6, 8))
+    with pytest.raises(TypeError):
+        P._ptr(t.float(), shape=(6, 9))
+    assert P._dt("f64") == P.F64 and P._dt("f32") == P.F32
+    for bad in ("float64", "fp64", "F64", "", None):
+        with pytest.raises(ValueError):
+            P._dt(bad)
+    with pytest.raises(ValueError):
+        P.Grid.create(np.zeros((6, 9)), dtype="double")
+    with pytest.raises(ValueError):
+        P.Grid.create(np.zeros(54))

@@ -210,6 +210,31 @@ def test_external_stream(gpu, orc):
     assert np.array_equal(out, ref)
 
 
+def test_wrong_shaped_buffers_are_rejected_by_the_binding(gpu, orc):
+    """reset / download / download_rows with a buffer of the wrong shape or
+    dtype raise before the C call (which would read or write out of bounds);
+    the handle stays usable and unchanged."""
+    init = SI.random_edges(20, 33, seed=4)
+    ref = init.copy()
+    orc.iterate(ref, 1.5, 3)
+    with gpu.Grid.create(init) as g:
+        g.iterate(1.5, 3)
+        for bad in (lambda: g.reset(np.zeros((22, 34))), lambda: g.reset(np.zeros((35, 22))),
+                    lambda: g.download(np.zeros((22, 36))), lambda: g.download(np.zeros(22 * 35)),
+                    lambda: g.download_rows(3, 9, np.zeros((5, 35))), lambda: g.download_rows(3, 9, np.zeros((6, 34)))):
+            with pytest.raises(ValueError):
+                bad()
+        with pytest.raises(TypeError):
+            g.download(np.zeros((22, 35), dtype=np.float32))
+        assert np.array_equal(g.download(), ref)
+    with gpu.Grid3D(SI.random_field3d(4, 5, 6, seed=1)) as g3:
+        with pytest.raises(ValueError):
+            g3.download(np.zeros((6, 7, 9)))
+        with pytest.raises(TypeError):
+            g3.download(np.zeros((6, 7, 8), dtype=np.float32))
+        assert g3.download().shape == (6, 7, 8)
+
+
 def test_invalid_calls_leave_handle_usable(gpu):
     init = SI.north_hot(10, 10, 1.0)
     with gpu.Grid.create(init) as g:
