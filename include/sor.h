@@ -215,7 +215,9 @@ int sor_variant_solve(sor_grid* g, const sor_variant* v, double omega, double to
  * Kernels (sor3d_set_kernel): SOR_KERNEL_NATURAL (two in-place colour
  * phases) or SOR_KERNEL_FUSED (the default: one HBM pass per iteration, a
  * z-plane wavefront over TMA-staged planes, src -> dst, two planes per CTA
- * barrier); bitwise equal.                                                  */
+ * barrier); bitwise equal.  The handle lives on the CUDA device current at
+ * sor3d_create; later calls run there whatever device is current and
+ * restore the caller's device on return (as the 2-D handles do).           */
 typedef struct sor3d_grid sor3d_grid;
 int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const double* init, sor_dtype dt);
 int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_change);

@@ -33,6 +33,7 @@ struct sor3d_grid {
   double* scratch = nullptr;
   bool failed = false, have_elapsed = false;
   double elapsed_ms = 0.0;
+  int device = 0;               // the device current at sor3d_create: every later call runs on it
 };
 
 namespace {
@@ -283,6 +284,22 @@ int usable3(sor3d_grid* g) {
 
 }  // namespace
 
+namespace {
+// Every call on a handle runs on the handle's device and restores the
+// caller's current device afterwards (as DevGuard in sor_api.cu).
+struct DevGuard3 {
+  int prev = -1;
+  bool changed = false;
+  explicit DevGuard3(const sor3d_grid* g) {
+    if (g && cudaGetDevice(&prev) == cudaSuccess && prev != g->device)
+      changed = cudaSetDevice(g->device) == cudaSuccess;
+  }
+  ~DevGuard3() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 extern "C" {
 
 int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const double* init, sor_dtype dt) {
@@ -306,6 +323,7 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
   if (!on_dev && !host_all_finite(init, n))
     return set_error3(nullptr, SOR_E_INVAL, "init contains non-finite values");
   sor3d_grid* g = new sor3d_grid();
+  g->device = dev;
   g->nz = nz;
   g->ny = ny;
   g->nx = nx;
@@ -371,6 +389,7 @@ int sor3d_create(sor3d_grid** out, int64_t nz, int64_t ny, int64_t nx, const dou
 
 int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_change) {
   if (int rc = usable3(g); rc < 0) return rc;
+  DevGuard3 dg(g);
   if (!(omega > 0.0 && omega < 2.0)) return set_error3(nullptr, SOR_E_INVAL, "omega must satisfy 0 < omega < 2");
   if (iters < 0) return set_error3(nullptr, SOR_E_INVAL, "iters must be >= 0");
   bool conv = false;
@@ -382,6 +401,7 @@ int sor3d_iterate(sor3d_grid* g, double omega, int64_t iters, double* last_max_c
 int sor3d_solve(sor3d_grid* g, double omega, double tol, int64_t maxit, int64_t check_every, int64_t* iters_out,
                 double* max_change_out) {
   if (int rc = usable3(g); rc < 0) return rc;
+  DevGuard3 dg(g);
   if (!(omega > 0.0 && omega < 2.0)) return set_error3(nullptr, SOR_E_INVAL, "omega must satisfy 0 < omega < 2");
   if (!(tol > 0.0) || !std::isfinite(tol)) return set_error3(nullptr, SOR_E_INVAL, "tol must be finite and > 0");
   if (maxit < 1 || check_every < 1 || check_every > maxit)
@@ -396,6 +416,7 @@ int sor3d_solve(sor3d_grid* g, double omega, double tol, int64_t maxit, int64_t 
 
 int sor3d_download(sor3d_grid* g, double* out) {
   if (int rc = usable3(g); rc < 0) return rc;
+  DevGuard3 dg(g);
   if (!out) return set_error3(nullptr, SOR_E_INVAL, "out is NULL");
   const int64_t w = g->nx + 2, nrow = (g->nz + 2) * (g->ny + 2);
   if (g->dt == SOR_F64) {
@@ -427,6 +448,7 @@ int sor3d_last_elapsed_ms(const sor3d_grid* g, double* ms) {
 
 void sor3d_destroy(sor3d_grid* g) {
   if (!g) return;
+  DevGuard3 dg(g);
   if (g->stream) cudaStreamSynchronize(g->stream);
   free3d(g);
 }
